@@ -1,0 +1,166 @@
+"""Standard FEM assembly / application of the system matrix A (oracle; test infra).
+
+This is the DEFINITION the DoGIP apply must reproduce:
+  WP  A_ij = int m phi_j phi_i          (eq:linsys_gp)
+  EL  A_ij = int M grad phi_j . grad phi_i  (eq:linsys_se)
+evaluated element by element with the contract rule Q (reading L10):
+  WP  K_T,ij = |det R_T| sum_q w_q m(F_T xq) phi_i(xq) phi_j(xq)
+  EL  K_T,ij = |det R_T| sum_q w_q (R_T^-T grad phi_i)^T M(F_T xq) (R_T^-T grad phi_j)
+(chain rule eq:bas_deriv), A = sum_T P_T^T K_T P_T.
+Never uses double-grid weights.
+
+Routes: CSR (scipy.sparse) for small meshes; element route (y = sum_T
+P_T^T K_T P_T u, the "alternative approaches" form of P:66-75) for big meshes;
+``apply_rows`` computes selected entries of A u one by one for full-size
+sampled parity.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import coefficients as coefs
+from .mesh import Mesh, affine_maps, boundary_mask, dof_map, dof_lattice, structured_mesh
+from .quadrature import contract_n1d, simplex_rule
+from .reference import eval_basis, eval_grad
+
+FORM_WP, FORM_EL = 0, 1
+
+
+class ElementData:
+    """Per-mesh precomputation shared by the routes (geometry, l_T, tables)."""
+
+    def __init__(self, mesh: Mesh, p: int, n1d: int | None = None):
+        self.mesh, self.p, self.d = mesh, p, mesh.d
+        self.R, self.S, self.det, self.Rinv = affine_maps(mesh)
+        self.lT = dof_map(mesh, p)
+        self.qp, self.qw = simplex_rule(mesh.d, n1d or contract_n1d(p))
+        self.Phi = eval_basis(mesh.d, p, self.qp)          # (nq, V_T)
+        self.dPhi = eval_grad(mesh.d, p, self.qp)          # (nq, V_T, d)
+        self.ndof = (p * mesh.N + 1) ** mesh.d
+
+    def element_matrices(self, form: int, coef, sl: slice) -> np.ndarray:
+        """K_T for elements in ``sl`` -> (nb, V_T, V_T)."""
+        d = self.d
+        R, S, det, Rinv = self.R[sl], self.S[sl], self.det[sl], self.Rinv[sl]
+        nb, nq = R.shape[0], self.qp.shape[0]
+        x = np.einsum("eij,qj->eqi", R, self.qp) + S[:, None, :]      # F_T(xq)
+        cell = np.repeat(self.mesh.cell[sl], nq)
+        c = coefs.evaluate(coef, d, x.reshape(-1, d), cell)
+        scale = np.abs(det)[:, None] * self.qw[None, :]               # (nb, nq)
+        if form == FORM_WP:
+            if c.ndim != 1:
+                raise ValueError("WP needs a scalar coefficient")
+            wq = scale * c.reshape(nb, nq)
+            return np.einsum("eq,qi,qj->eij", wq, self.Phi, self.Phi)
+        Mq = coefs.as_tensor(c, d).reshape(nb, nq, d, d)
+        # physical gradients: grad phi = R^-T grad_hat phi  (eq:bas_deriv)
+        G = np.einsum("epr,qlp->eqlr", Rinv, self.dPhi)               # (nb,nq,V_T,d)
+        MG = np.einsum("eqrs,eqls->eqlr", Mq, G)
+        return np.einsum("eq,eqir,eqjr->eij", scale, G, MG)
+
+    def chunks(self, chunk: int = 16384):
+        ne = self.mesh.n_elem
+        for s in range(0, ne, chunk):
+            yield slice(s, min(ne, s + chunk))
+
+
+def assemble_csr(ed: ElementData, form: int, coef) -> sp.csr_matrix:
+    """A = sum_T P_T^T K_T P_T as a CSR matrix."""
+    rows, cols, vals = [], [], []
+    for sl in ed.chunks():
+        K = ed.element_matrices(form, coef, sl)
+        l = ed.lT[sl]
+        rows.append(np.repeat(l, l.shape[1], axis=1).ravel())
+        cols.append(np.tile(l, (1, l.shape[1])).ravel())
+        vals.append(K.ravel())
+    A = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(ed.ndof, ed.ndof))
+    return A.tocsr()
+
+
+def apply_elementwise(ed: ElementData, form: int, coef, u: np.ndarray,
+                      dirichlet: bool = False) -> np.ndarray:
+    """y = sum_T P_T^T K_T P_T u without forming A; with
+    ``dirichlet`` the symmetric-elimination operator of ``dirichlet_apply``."""
+    mask = boundary_mask(ed.d, ed.mesh.N, ed.p) if dirichlet else None
+    uu = np.where(mask, 0.0, u) if dirichlet else u
+    y = np.zeros(ed.ndof)
+    for sl in ed.chunks():
+        K = ed.element_matrices(form, coef, sl)
+        l = ed.lT[sl]
+        yl = np.einsum("eij,ej->ei", K, uu[l])
+        y += np.bincount(l.ravel(), weights=yl.ravel(), minlength=ed.ndof)
+    if dirichlet:
+        y[mask] = u[mask]
+    return y
+
+
+def elements_containing(ed: ElementData, dof: int) -> np.ndarray:
+    """Elements whose closure contains global DoF ``dof`` (structured search)."""
+    d, N, p = ed.d, ed.mesh.N, ed.p
+    lat = dof_lattice(d, N, p)[dof]
+    cand_axes = []
+    for a in range(d):
+        X = int(lat[a])
+        cs = {X // p, (X - 1) // p} if X % p == 0 else {X // p}
+        cand_axes.append([c for c in cs if 0 <= c < N])
+    ns = 2 if d == 2 else 6
+    out = []
+    for cc in np.array(np.meshgrid(*cand_axes, indexing="ij")).reshape(d, -1).T:
+        cell = int(sum(int(cc[a]) * N ** a for a in range(d)))
+        for s in range(ns):
+            e = ns * cell + s
+            if dof in ed.lT[e]:
+                out.append(e)
+    return np.array(out, dtype=np.int64)
+
+
+def apply_rows(ed: ElementData, form: int, coef, u: np.ndarray, rows) -> np.ndarray:
+    """(A u)_i for the given rows only: sum over T containing i of (K_T u_T)_i."""
+    out = np.empty(len(rows))
+    for n, i in enumerate(rows):
+        els = elements_containing(ed, int(i))
+        acc = 0.0
+        for e in els:
+            K = ed.element_matrices(form, coef, slice(e, e + 1))[0]
+            li = int(np.nonzero(ed.lT[e] == i)[0][0])
+            acc += K[li] @ u[ed.lT[e]]
+        out[n] = acc
+    return out
+
+
+def load_vector(ed: ElementData, f: float = 1.0, dirichlet: bool = False) -> np.ndarray:
+    """b_i = int f phi_i (eq:linsys_gp P:207, eq:linsys_se P:337), f constant;
+    zeroed on boundary DoFs when ``dirichlet`` (reading L14)."""
+    s = ed.Phi.T @ ed.qw                                  # int_ref phi_i
+    be = f * np.abs(ed.det)[:, None] * s[None, :]
+    b = np.bincount(ed.lT.ravel(), weights=be.ravel(), minlength=ed.ndof)
+    if dirichlet:
+        b[boundary_mask(ed.d, ed.mesh.N, ed.p)] = 0.0
+    return b
+
+
+def load_vector_fn(ed: ElementData, f) -> np.ndarray:
+    """b_i = int f phi_i for a callable f(x) (x: (n, d) physical points), by the
+    contract rule (eq:linsys_gp P:207).  Used by the polynomial-reproduction pins."""
+    d = ed.d
+    b = np.zeros(ed.ndof)
+    for sl in ed.chunks():
+        R, S, det = ed.R[sl], ed.S[sl], ed.det[sl]
+        x = np.einsum("eij,qj->eqi", R, ed.qp) + S[:, None, :]
+        fx = f(x.reshape(-1, d)).reshape(x.shape[0], -1)
+        be = np.einsum("eq,q,qi->ei", fx * np.abs(det)[:, None], ed.qw, ed.Phi)
+        b += np.bincount(ed.lT[sl].ravel(), weights=be.ravel(), minlength=ed.ndof)
+    return b
+
+
+def dirichlet_matrix(A: sp.csr_matrix, mask: np.ndarray) -> sp.csr_matrix:
+    """Symmetric elimination (reading L14): rows/cols of boundary DoFs replaced
+    by the identity, A_D = D A D + (I - D), D = diag(interior)."""
+    D = sp.diags((~mask).astype(np.float64))
+    return (D @ A @ D + sp.diags(mask.astype(np.float64))).tocsr()
+
+
+def build(d: int, N: int, p: int, vertices=None, n1d=None) -> ElementData:
+    return ElementData(structured_mesh(d, N, vertices), p, n1d)
