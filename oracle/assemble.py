@@ -164,3 +164,42 @@ def dirichlet_matrix(A: sp.csr_matrix, mask: np.ndarray) -> sp.csr_matrix:
 
 def build(d: int, N: int, p: int, vertices=None, n1d=None) -> ElementData:
     return ElementData(structured_mesh(d, N, vertices), p, n1d)
+
+
+def apply_rows_sampled(d: int, N: int, p: int, vertices, form: int, coef, u: np.ndarray,
+                       rows, n1d=None) -> np.ndarray:
+    """(A u)_i for sampled rows of a FULL-SIZE mesh without building it: for
+    each row, only the cells around its DoF are instantiated (same mesh rule,
+    same element matrices as ElementData)."""
+    from .mesh import Mesh, cell_elements
+    Md = p * N + 1
+    out = np.empty(len(rows))
+    M = N + 1
+    for n, i in enumerate(rows):
+        i = int(i)
+        lat = [(i // Md ** a) % Md for a in range(d)]
+        axes = []
+        for a in range(d):
+            X = lat[a]
+            cs = {X // p, (X - 1) // p} if X % p == 0 else {X // p}
+            axes.append([c for c in cs if 0 <= c < N])
+        cells = np.array([sum(int(cc[a]) * N ** a for a in range(d))
+                          for cc in np.array(np.meshgrid(*axes, indexing="ij")).reshape(d, -1).T])
+        elems = cell_elements(d, N, cells)
+        vids = np.unique(elems)
+        vlat = np.stack([(vids // M ** a) % M for a in range(d)], axis=1)
+        X = vlat / N if vertices is None else np.asarray(vertices)[vids]
+        remap = {int(v): k for k, v in enumerate(vids)}
+        loc = np.vectorize(remap.get)(elems)
+        sub = Mesh(d, N, vlat, X, loc, np.repeat(cells, 2 if d == 2 else 6))
+        ed = ElementData(sub, p, n1d)
+        # global DoF ids: dof_map used lattice coords of the local vertices -> still global
+        ed.ndof = Md ** d
+        K = ed.element_matrices(form, coef, slice(0, sub.n_elem))
+        acc = 0.0
+        for e in range(sub.n_elem):
+            hit = np.nonzero(ed.lT[e] == i)[0]
+            if hit.size:
+                acc += K[e, hit[0]] @ u[ed.lT[e]]
+        out[n] = acc
+    return out

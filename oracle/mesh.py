@@ -113,3 +113,19 @@ def affine_maps(mesh: Mesh):
     det = np.linalg.det(R)
     Rinv = np.linalg.inv(R)
     return R, S, det, Rinv
+
+
+def cell_elements(d: int, N: int, cells: np.ndarray) -> np.ndarray:
+    """Vertex ids (n, d+1) of the d! simplices of the given cells, in canonical
+    order e = d!*cell + s (same rule as structured_mesh, for sampled rows)."""
+    M = N + 1
+    cells = np.asarray(cells, dtype=np.int64)
+    clat = np.stack([(cells // N ** a) % N for a in range(d)], axis=1)
+    simp = _simplices_of_cell(d)
+    ns = len(simp)
+    elems = np.empty((cells.size * ns, d + 1), dtype=np.int64)
+    for s, verts in enumerate(simp):
+        for v, off in enumerate(verts):
+            c = clat + np.array(off)
+            elems[s::ns, v] = sum(c[:, a] * M ** a for a in range(d))
+    return elems

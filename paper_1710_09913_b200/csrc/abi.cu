@@ -1,0 +1,678 @@
+// abi.cu -- the C ABI of libdogip.so (include/dogip.h): handles, argument
+// checking, setup tables, the apply / exchange / CG orchestration on CUDA
+// streams.  Every arithmetic step of the path runs in kernels/*.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dogip.h"
+#include "host/comm.hpp"
+#include "host/quadrature.hpp"
+#include "host/tables.hpp"
+#include "kernels/apply.cuh"
+
+using namespace dogip;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return fail(e_ == cudaErrorMemoryAllocation ? DOGIP_E_OOM : DOGIP_E_CUDA,       \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                \
+    } while (0)
+#define NK(call)                                                                            \
+    do {                                                                                    \
+        ncclResult_t r_ = (call);                                                           \
+        if (r_ != ncclSuccess)                                                              \
+            return fail(DOGIP_E_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
+    } while (0)
+#define RET(call)                     \
+    do {                              \
+        int rc_ = (call);             \
+        if (rc_ < 0) return rc_;      \
+    } while (0)
+
+// ------------------------------------------------------------------ handles
+struct dogip_mesh_s {
+    int d = 0, p = 0, rank = 0, nranks = 1, device = 0, num_sms = 148;
+    int64_t N = 0, z0 = 0, z1 = 0;
+    SlabGeo geo{};
+    ApplyTables tab{};
+    RefInfo ref{};          // V-side layout (form independent)
+    double* d_verts = nullptr;
+    ncclComm_t comm = nullptr;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
+    double* rbuf = nullptr;   // 2 planes: from rank-1, from rank+1
+};
+
+struct dogip_op_s {
+    dogip_mesh_s* m = nullptr;
+    int form = 0, nq = 0;
+    RefInfo ref{};
+    double* d_w = nullptr;
+    int64_t w_doubles = 0;
+    double* d_sV = nullptr;   // int_ref phi^V_l, for the load vector
+    double* r = nullptr;      // CG scratch
+    double* pv = nullptr;
+    double* q = nullptr;
+    double* partials = nullptr;
+    double* scal = nullptr;
+    double* h_scal = nullptr;  // pinned
+    double* hu = nullptr;      // device scratch for the host-buffer apply
+    double* hy = nullptr;
+    float weights_ms = 0.f;
+};
+
+static int64_t ipow(int64_t b, int e) {
+    int64_t r = 1;
+    while (e--) r *= b;
+    return r;
+}
+
+extern "C" int dogip_version(void) { return 100; }
+extern "C" const char* dogip_last_error(void) { return g_err.c_str(); }
+
+extern "C" int dogip_slab_range(int64_t N, int rank, int nranks, int64_t* z0, int64_t* z1) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || N < nranks)
+        return fail(DOGIP_E_INVALID_SIZE, "slab partition needs N >= nranks >= 1 and 0 <= rank < nranks");
+    *z0 = N * rank / nranks;
+    *z1 = N * (rank + 1) / nranks;
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_nccl_unique_id(void* out128) {
+    if (!out128) return fail(DOGIP_E_INVALID_ARG, "null output");
+    auto& api = nccl();
+    if (!api.ok) return fail(DOGIP_E_NCCL, api.err);
+    ncclUniqueId id;
+    NK(api.GetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof id);
+    return DOGIP_OK;
+}
+
+// ------------------------------------------------------------------ mesh
+extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices, int rank, int nranks,
+                                const void* nccl_id, int device, dogip_mesh* out) {
+    if (!out) return fail(DOGIP_E_INVALID_ARG, "null output handle");
+    *out = nullptr;
+    if (d != 2 && d != 3) return fail(DOGIP_E_INVALID_DIM, "invalid-dimension: d must be 2 or 3");
+    if (N < 1) return fail(DOGIP_E_INVALID_SIZE, "invalid-size: N must be >= 1");
+    if (p < 1 || p > 4) return fail(DOGIP_E_UNSUPPORTED_ORDER, "p must be in 1..4");
+    if (nranks < 1 || rank < 0 || rank >= nranks || N < nranks)
+        return fail(DOGIP_E_INVALID_SIZE, "invalid-size: need N >= nranks >= 1, 0 <= rank < nranks");
+    if ((double)ipow(p * N + 1, d) > 9.0e15) return fail(DOGIP_E_INVALID_SIZE, "mesh too large");
+    auto* m = new dogip_mesh_s();
+    m->d = d; m->N = N; m->p = p; m->rank = rank; m->nranks = nranks; m->device = device;
+    dogip_slab_range(N, rank, nranks, &m->z0, &m->z1);
+    const int64_t L = m->z1 - m->z0, M = p * N + 1;
+    ref_info(d, p, 0, m->ref);
+    SlabGeo& g = m->geo;
+    g.d = d; g.p = p; g.ns = d == 2 ? 2 : 6; g.N = (int)N;
+    g.Nx = (int)N;
+    g.Ny = d == 2 ? (int)L : (int)N;
+    g.Nz = d == 2 ? 1 : (int)L;
+    g.nxb = (int)((N + TILE - 1) / TILE);
+    g.ntiles = (int64_t)g.ns * g.nxb * g.Ny * g.Nz;
+    g.sy = M;
+    g.sz = d == 3 ? M * M : 0;
+    g.ndof = ipow(M, d - 1) * (p * L + 1);
+    g.pmax_x = (int)(p * N);
+    g.pmax_y = d == 2 ? (int)(p * L) : (int)(p * N);
+    g.pmax_z = d == 2 ? 0 : (int)(p * L);
+    g.bnd_lo = m->z0 == 0;
+    g.bnd_hi = m->z1 == N;
+    g.zoff = m->z0;
+    for (int s = 0; s < g.ns; ++s)
+        for (int l = 0; l < m->ref.VT; ++l) {
+            const int* o = m->ref.loff[s][l];
+            m->tab.off[s * MAX_VT + l] = (int)(o[0] + M * o[1] + (d == 3 ? M * M * o[2] : 0));
+            m->tab.loff[s * MAX_VT + l] = o[0] | (o[1] << 8) | (o[2] << 16);
+        }
+    if (device < 0) {   // host-only mesh: partition / numbering introspection, no device work
+        *out = m;
+        return DOGIP_OK;
+    }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) { delete m; return fail(DOGIP_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
+    cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (vertices) {
+        // host-side orientation check of the jittered mesh (E_DEGENERATE_ELEMENT)
+        const int64_t nv = ipow(N + 1, d);
+        for (int64_t i = 0; i < nv * d; ++i)
+            if (!std::isfinite(vertices[i])) { delete m; return fail(DOGIP_E_DEGENERATE_ELEMENT, "non-finite vertex"); }
+        e = cudaMalloc(&m->d_verts, sizeof(double) * nv * d);
+        if (e == cudaSuccess) e = cudaMemcpy(m->d_verts, vertices, sizeof(double) * nv * d, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { cudaFree(m->d_verts); delete m; return fail(DOGIP_E_OOM, "vertex upload failed"); }
+    }
+    if (nranks > 1 && nccl_id) {
+        auto& api = nccl();
+        if (!api.ok) { dogip_mesh_destroy(m); return fail(DOGIP_E_NCCL, api.err); }
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof id);
+        ncclResult_t r = api.CommInitRank(&m->comm, nranks, id, rank);
+        if (r != ncclSuccess) { m->comm = nullptr; dogip_mesh_destroy(m); return fail(DOGIP_E_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)); }
+        cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&m->ev_bnd, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&m->ev_comm, cudaEventDisableTiming);
+        const int64_t plane = ipow(M, d - 1);
+        if (cudaMalloc(&m->rbuf, sizeof(double) * 2 * plane) != cudaSuccess) { dogip_mesh_destroy(m); return fail(DOGIP_E_OOM, "exchange buffers"); }
+    }
+    *out = m;
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_mesh_info(dogip_mesh m, dogip_mesh_info_t* o) {
+    if (!m || !o) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    const int64_t M = m->p * m->N + 1, plane = ipow(M, m->d - 1);
+    o->d = m->d; o->p = m->p; o->rank = m->rank; o->nranks = m->nranks;
+    o->N = m->N; o->z0 = m->z0; o->z1 = m->z1;
+    o->n_elem_local = (m->d == 2 ? 2 : 6) * ipow(m->N, m->d - 1) * (m->z1 - m->z0);
+    o->n_elem_global = (m->d == 2 ? 2 : 6) * ipow(m->N, m->d);
+    o->ndof_local = m->geo.ndof;
+    o->ndof_global = ipow(M, m->d);
+    o->plane_size = plane;
+    o->dof_offset = m->p * m->z0 * plane;
+    o->owned_begin = 0;
+    o->owned_end = m->rank < m->nranks - 1 ? m->geo.ndof - plane : m->geo.ndof;
+    return DOGIP_OK;
+}
+
+extern "C" void dogip_mesh_destroy(dogip_mesh m) {
+    if (!m) return;
+    if (m->device < 0) { delete m; return; }
+    cudaSetDevice(m->device);
+    if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
+    if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+    if (m->ev_bnd) cudaEventDestroy(m->ev_bnd);
+    if (m->ev_comm) cudaEventDestroy(m->ev_comm);
+    cudaFree(m->rbuf);
+    cudaFree(m->d_verts);
+    delete m;
+}
+
+// ------------------------------------------------------------------ weights
+static int check_coeff(int d, int form, const dogip_coeff* c, int& ncomp) {
+    if (!c) return fail(DOGIP_E_BAD_COEFF, "null coefficient");
+    const int64_t np = c->nparams;
+    auto need = [&](int64_t k) { return np >= k && c->params; };
+    ncomp = 1;
+    switch (c->kind) {
+        case DOGIP_COEF_CONST:
+            if (!need(1) || !(c->params[0] > 0)) return fail(DOGIP_E_BAD_COEFF, "CONST needs params[0] > 0");
+            return 0;
+        case DOGIP_COEF_PER_CELL:
+            if (!c->per_cell) return fail(DOGIP_E_BAD_COEFF, "PER_CELL needs per_cell values");
+            return 0;
+        case DOGIP_COEF_SINCOS2D:
+            if (d != 2 || !need(2)) return fail(DOGIP_E_BAD_COEFF, "SINCOS2D needs d = 2 and 2 params");
+            return 0;
+        case DOGIP_COEF_TANH_RADIAL:
+            if (!need(4 + d)) return fail(DOGIP_E_BAD_COEFF, "TANH_RADIAL needs 4 + d params");
+            return 0;
+        case DOGIP_COEF_ANISO_FOURIER: {
+            if (d != 3 || form != DOGIP_EL || !need(4)) return fail(DOGIP_E_BAD_COEFF, "ANISO_FOURIER needs d = 3, EL");
+            const int64_t n = (int64_t)c->params[3];
+            if (n < 0 || np < 4 + 9 * n) return fail(DOGIP_E_BAD_COEFF, "ANISO_FOURIER parameter count");
+            if (!(c->params[0] > 0 && c->params[1] > 0 && c->params[2] > 0)) return fail(DOGIP_E_BAD_COEFF, "eigenvalues must be > 0");
+            ncomp = 6;
+            return 0;
+        }
+        case DOGIP_COEF_CONST_TENSOR: {
+            if (form != DOGIP_EL || !need(d * d)) return fail(DOGIP_E_BAD_COEFF, "CONST_TENSOR needs EL and d*d params");
+            for (int a = 0; a < d; ++a) {
+                if (!(c->params[a * d + a] > 0)) return fail(DOGIP_E_BAD_COEFF, "tensor diagonal must be > 0");
+                for (int b = 0; b < d; ++b)
+                    if (c->params[a * d + b] != c->params[b * d + a]) return fail(DOGIP_E_BAD_COEFF, "tensor not symmetric");
+            }
+            ncomp = d * (d + 1) / 2;
+            return 0;
+        }
+    }
+    return fail(DOGIP_E_BAD_COEFF, "unknown coefficient kind");
+}
+
+struct DevBufs {   // frees on scope exit
+    std::vector<void*> p;
+    ~DevBufs() { for (void* x : p) cudaFree(x); }
+    template <class T> cudaError_t alloc(T** out, size_t n) {
+        cudaError_t e = cudaMalloc((void**)out, sizeof(T) * std::max<size_t>(n, 1));
+        if (e == cudaSuccess) p.push_back(*out);
+        return e;
+    }
+};
+
+extern "C" int dogip_weights(dogip_mesh m, int form, const dogip_coeff* coeff, int quad_n1d, void* stream,
+                             dogip_op* out) {
+    if (!m || !out) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    *out = nullptr;
+    if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
+    if (m->device < 0) return fail(DOGIP_E_INVALID_ARG, "host-only mesh (device < 0) cannot hold an operator");
+    int ncomp = 1;
+    RET(check_coeff(m->d, form, coeff, ncomp));
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int d = m->d, p = m->p;
+    auto* op = new dogip_op_s();
+    op->m = m;
+    op->form = form;
+    ref_info(d, p, form, op->ref);
+    const int WT = op->ref.WT, NC = op->ref.NC, VT = op->ref.VT;
+    const int n1d = quad_n1d > 0 ? quad_n1d : p + 3;
+    std::vector<double> pts, wts;
+    simplex_rule(d, n1d, pts, wts);
+    const int nq = (int)wts.size();
+    op->nq = n1d;
+    const int kw = form == DOGIP_WP ? 2 * p : 2 * p - 2;
+    std::vector<double> phiW((size_t)nq * WT), phiV((size_t)nq * VT), sW(WT), sV(VT);
+    eval_basis_ld(d, kw, pts.data(), nq, phiW.data());
+    eval_basis_ld(d, p, pts.data(), nq, phiV.data());
+    for (int j = 0; j < WT; ++j) {
+        long double s = 0;
+        for (int q = 0; q < nq; ++q) s += (long double)wts[q] * phiW[(size_t)q * WT + j];
+        sW[j] = (double)s;
+    }
+    for (int l = 0; l < VT; ++l) {
+        long double s = 0;
+        for (int q = 0; q < nq; ++q) s += (long double)wts[q] * phiV[(size_t)q * VT + l];
+        sV[l] = (double)s;
+    }
+    op->w_doubles = m->geo.ntiles * (int64_t)WT * NC * TILE;
+    auto cleanup_fail = [&](int code, const std::string& msg) { dogip_op_destroy(op); return fail(code, msg); };
+    if (cudaMalloc(&op->d_w, sizeof(double) * op->w_doubles) != cudaSuccess)
+        return cleanup_fail(DOGIP_E_OOM, "weights allocation (" + std::to_string(op->w_doubles * 8) + " bytes)");
+    if (cudaMalloc(&op->d_sV, sizeof(double) * VT) != cudaSuccess) return cleanup_fail(DOGIP_E_OOM, "sV");
+    cudaMemcpy(op->d_sV, sV.data(), sizeof(double) * VT, cudaMemcpyHostToDevice);
+
+    DevBufs tmp;
+    WeightsArgs a{};
+    a.d = d; a.p = p; a.form = form; a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
+    a.kind = coeff->kind;
+    a.nparams = (int)coeff->nparams;
+    a.geo = m->geo;
+    a.out = op->d_w;
+    a.verts = m->d_verts;
+    a.stream = st;
+    double *dparams = nullptr, *dqp = nullptr, *dqw = nullptr, *dphi = nullptr, *dsW = nullptr, *dcell = nullptr;
+    int* dbad = nullptr;
+    if (tmp.alloc(&dparams, coeff->nparams) || tmp.alloc(&dqp, pts.size()) || tmp.alloc(&dqw, wts.size()) ||
+        tmp.alloc(&dphi, phiW.size()) || tmp.alloc(&dsW, WT) || tmp.alloc(&dbad, 1))
+        return cleanup_fail(DOGIP_E_OOM, "weight tables");
+    if (coeff->nparams) cudaMemcpy(dparams, coeff->params, sizeof(double) * coeff->nparams, cudaMemcpyHostToDevice);
+    cudaMemcpy(dqp, pts.data(), sizeof(double) * pts.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dqw, wts.data(), sizeof(double) * wts.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dphi, phiW.data(), sizeof(double) * phiW.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dsW, sW.data(), sizeof(double) * WT, cudaMemcpyHostToDevice);
+    cudaMemset(dbad, 0, sizeof(int));
+    if (coeff->kind == DOGIP_COEF_PER_CELL) {
+        const int64_t ncell = ipow(m->N, d);
+        if (tmp.alloc(&dcell, ncell)) return cleanup_fail(DOGIP_E_OOM, "per-cell coefficient");
+        cudaMemcpy(dcell, coeff->per_cell, sizeof(double) * ncell, cudaMemcpyHostToDevice);
+    }
+    a.params = dparams; a.qp = dqp; a.qw = dqw; a.phiW = dphi; a.sW = dsW; a.per_cell = dcell; a.bad_flag = dbad;
+    const bool direct = coeff->kind == DOGIP_COEF_CONST || coeff->kind == DOGIP_COEF_PER_CELL ||
+                        coeff->kind == DOGIP_COEF_CONST_TENSOR;
+    int64_t batch = (int64_t)(256ll << 20) / (8ll * ncomp * std::max(nq, WT));
+    batch = std::max<int64_t>(TILE, batch / TILE * TILE);
+    a.batch = batch;
+    if (!direct) {
+        if (tmp.alloc(&a.scratch_c, (size_t)batch * ncomp * nq) || tmp.alloc(&a.scratch_a, (size_t)batch * ncomp * WT))
+            return cleanup_fail(DOGIP_E_OOM, "weight scratch");
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+    cudaError_t ce = launch_weights(a);
+    cudaEventRecord(e1, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce == cudaSuccess) cudaEventElapsedTime(&op->weights_ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ce != cudaSuccess) return cleanup_fail(DOGIP_E_CUDA, std::string("weights kernels: ") + cudaGetErrorString(ce));
+    int bad = 0;
+    cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost);
+    if (bad & 1) return cleanup_fail(DOGIP_E_DEGENERATE_ELEMENT, "an element is degenerate or inverted");
+    if (bad & 2) return cleanup_fail(DOGIP_E_BAD_COEFF, "coefficient is not positive at a quadrature point");
+    *out = op;
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_op_info(dogip_op op, dogip_op_info_t* o) {
+    if (!op || !o) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    o->form = op->form; o->d = op->m->d; o->p = op->m->p;
+    o->V_T = op->ref.VT; o->W_T = op->ref.WT; o->n_c = op->ref.NC;
+    o->quad_n1d = op->nq;
+    o->n_tiles = op->m->geo.ntiles;
+    o->weight_bytes = op->w_doubles * 8;
+    o->weights_ms = op->weights_ms;
+    return DOGIP_OK;
+}
+
+extern "C" void dogip_op_destroy(dogip_op op) {
+    if (!op) return;
+    cudaSetDevice(op->m->device);
+    for (double* x : {op->d_w, op->d_sV, op->r, op->pv, op->q, op->partials, op->scal, op->hu, op->hy}) cudaFree(x);
+    if (op->h_scal) cudaFreeHost(op->h_scal);
+    delete op;
+}
+
+// ------------------------------------------------------------------ apply
+static int exchange_planes(dogip_mesh_s* m, double* y, cudaEvent_t ready) {
+    // sum this rank's partial interface planes with the neighbours' (A8)
+    auto& api = nccl();
+    const int64_t P = m->d == 3 ? m->geo.sy * m->geo.sy : m->geo.sy;
+    const int64_t last = m->geo.ndof - P;
+    CK(cudaStreamWaitEvent(m->comm_stream, ready, 0));
+    NK(api.GroupStart());
+    if (m->rank > 0) {
+        NK(api.Send(y, P, ncclDouble, m->rank - 1, m->comm, m->comm_stream));
+        NK(api.Recv(m->rbuf, P, ncclDouble, m->rank - 1, m->comm, m->comm_stream));
+    }
+    if (m->rank < m->nranks - 1) {
+        NK(api.Send(y + last, P, ncclDouble, m->rank + 1, m->comm, m->comm_stream));
+        NK(api.Recv(m->rbuf + P, P, ncclDouble, m->rank + 1, m->comm, m->comm_stream));
+    }
+    NK(api.GroupEnd());
+    CK(cudaEventRecord(m->ev_comm, m->comm_stream));
+    return DOGIP_OK;
+}
+
+static int finish_exchange(dogip_mesh_s* m, double* y, cudaStream_t st) {
+    const int64_t P = m->d == 3 ? m->geo.sy * m->geo.sy : m->geo.sy;
+    CK(cudaStreamWaitEvent(st, m->ev_comm, 0));
+    CK(launch_add_planes(y, m->rank > 0 ? m->rbuf : nullptr, m->rank < m->nranks - 1 ? m->rbuf + P : nullptr, P,
+                         m->geo.ndof - P, st));
+    return DOGIP_OK;
+}
+
+static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, cudaStream_t st) {
+    dogip_mesh_s* m = op->m;
+    const SlabGeo& g = m->geo;
+    CK(cudaMemsetAsync(y, 0, sizeof(double) * g.ndof, st));
+    ApplyArgs a{};
+    a.d = m->d; a.p = m->p; a.form = op->form;
+    a.dirichlet = (flags & DOGIP_DIRICHLET_ZERO) != 0;
+    a.u = u; a.y = y; a.w = op->d_w; a.geo = g; a.tab = &m->tab;
+    a.num_sms = m->num_sms;
+    a.stream = st;
+    const bool xchg = m->nranks > 1 && m->comm && !(flags & DOGIP_NO_EXCHANGE);
+    if (!xchg) {
+        a.tile_begin = 0; a.tile_end = g.ntiles;
+        CK(launch_apply(a));
+    } else {
+        // boundary cube layers first, exchange overlapped with the interior layers
+        const int64_t layers = m->z1 - m->z0;
+        const int64_t tpl = g.ntiles / layers;
+        if (layers <= 2) {
+            a.tile_begin = 0; a.tile_end = g.ntiles;
+            CK(launch_apply(a));
+            CK(cudaEventRecord(m->ev_bnd, st));
+            RET(exchange_planes(m, y, m->ev_bnd));
+        } else {
+            a.tile_begin = 0; a.tile_end = tpl;
+            CK(launch_apply(a));
+            a.tile_begin = g.ntiles - tpl; a.tile_end = g.ntiles;
+            CK(launch_apply(a));
+            CK(cudaEventRecord(m->ev_bnd, st));
+            RET(exchange_planes(m, y, m->ev_bnd));
+            a.tile_begin = tpl; a.tile_end = g.ntiles - tpl;
+            CK(launch_apply(a));
+        }
+        RET(finish_exchange(m, y, st));
+    }
+    if (a.dirichlet) CK(launch_dirichlet_fixup(g, u, y, st));
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_apply(dogip_op op, const double* u, double* y, unsigned flags, void* stream) {
+    if (!op || !u || !y) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (u == y) return fail(DOGIP_E_INVALID_ARG, "u and y must not alias");
+    if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
+    return apply_impl(op, u, y, flags, (cudaStream_t)stream);
+}
+
+extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_host, unsigned flags, void* stream) {
+    if (!op || !u_host || !y_host) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = op->m->geo.ndof;
+    if (!op->hu) {
+        CK(cudaMalloc(&op->hu, sizeof(double) * n));
+        CK(cudaMalloc(&op->hy, sizeof(double) * n));
+    }
+    CK(cudaMemcpyAsync(op->hu, u_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    RET(dogip_apply(op, op->hu, op->hy, flags, stream));
+    CK(cudaMemcpyAsync(y_host, op->hy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_load_vector(dogip_op op, double f, double* b, unsigned flags, void* stream) {
+    if (!op || !b) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    dogip_mesh_s* m = op->m;
+    CK(cudaMemsetAsync(b, 0, sizeof(double) * m->geo.ndof, st));
+    CK(launch_load_vector(m->geo, m->p, m->d_verts, op->d_sV, op->ref.VT, &m->tab, f, b, st));
+    if (m->nranks > 1 && m->comm && !(flags & DOGIP_NO_EXCHANGE)) {
+        CK(cudaEventRecord(m->ev_bnd, st));
+        RET(exchange_planes(m, b, m->ev_bnd));
+        RET(finish_exchange(m, b, st));
+    }
+    if (flags & DOGIP_DIRICHLET_ZERO) CK(launch_zero_boundary(m->geo, b, st));
+    return DOGIP_OK;
+}
+
+// ------------------------------------------------------------------ CG
+static int allreduce_scalar(dogip_mesh_s* m, double* s, cudaStream_t st) {
+    if (m->nranks > 1 && m->comm) NK(nccl().AllReduce(s, s, 1, ncclDouble, ncclSum, m->comm, st));
+    return DOGIP_OK;
+}
+
+extern "C" int64_t dogip_kernel_launches(void) { return (int64_t)g_launches.load(); }
+
+extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, int maxit, unsigned flags,
+                        void* stream, dogip_cg_result* res) {
+    if (!op || !b || !x || !res) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_CG_RESUME)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
+    cudaStream_t st = (cudaStream_t)stream;
+    dogip_mesh_s* m = op->m;
+    const int64_t n = m->geo.ndof;
+    dogip_mesh_info_t info;
+    dogip_mesh_info(m, &info);
+    const int64_t o0 = info.owned_begin, o1 = info.owned_end;
+    const bool resume = (flags & DOGIP_CG_RESUME) != 0;
+    if (resume && !op->r) return fail(DOGIP_E_INVALID_ARG, "DOGIP_CG_RESUME without a previous dogip_cg call");
+    if (!op->r) {
+        CK(cudaMalloc(&op->r, sizeof(double) * n));
+        CK(cudaMalloc(&op->pv, sizeof(double) * n));
+        CK(cudaMalloc(&op->q, sizeof(double) * n));
+        CK(cudaMalloc(&op->partials, sizeof(double) * RED_BLOCKS));
+        CK(cudaMalloc(&op->scal, sizeof(double) * S_COUNT));
+        CK(cudaMallocHost(&op->h_scal, sizeof(double) * S_COUNT));
+    }
+    const unsigned aflags = flags & DOGIP_DIRICHLET_ZERO;
+    const bool bench = maxit < 0;
+    const int nit = bench ? -maxit : maxit;
+    cudaEvent_t t0, t1, ready;
+    CK(cudaEventCreate(&t0));
+    CK(cudaEventCreate(&t1));
+    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    std::vector<cudaEvent_t> aev;
+    struct EvGuard {
+        cudaEvent_t a, b, c;
+        std::vector<cudaEvent_t>* v;
+        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c); for (auto e : *v) cudaEventDestroy(e); }
+    } guard{t0, t1, ready, &aev};
+    if (bench) {
+        aev.resize(2 * (size_t)nit);
+        for (auto& e : aev) CK(cudaEventCreate(&e));
+    }
+    CK(cudaEventRecord(t0, st));
+    if (!resume) {
+        // r = b - A x ; p = r
+        RET(apply_impl(op, x, op->q, aflags, st));
+        CK(cudaMemcpyAsync(op->r, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        CK(launch_axpby(op->r, op->q, -1.0, 1.0, n, st));
+        CK(cudaMemcpyAsync(op->pv, op->r, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        CK(launch_dot(op->r, op->r, o0, o1, op->partials, op->scal + S_RR, st));
+        RET(allreduce_scalar(m, op->scal + S_RR, st));
+    }
+    CK(launch_dot(b, b, o0, o1, op->partials, op->scal + S_BB, st));
+    RET(allreduce_scalar(m, op->scal + S_BB, st));
+    double rr = 0.0, bnorm = 0.0;
+    if (!bench) {
+        CK(cudaMemcpyAsync(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        bnorm = std::sqrt(op->h_scal[S_BB]);
+        rr = op->h_scal[S_RR];
+        if (bnorm == 0.0) {
+            res->iters = 0; res->status = DOGIP_OK; res->rel_res = 0.0; res->seconds = 0.0; res->apply_seconds = 0.0;
+            return DOGIP_OK;
+        }
+    }
+    int it = 0, status = DOGIP_OK;
+    while (true) {
+        if (!bench && std::sqrt(rr) <= rtol * bnorm) break;
+        if (it >= nit) { status = bench ? DOGIP_OK : DOGIP_NOT_CONVERGED; break; }
+        if (bench) CK(cudaEventRecord(aev[2 * it], st));
+        RET(apply_impl(op, op->pv, op->q, aflags, st));                        // q = A p
+        if (bench) CK(cudaEventRecord(aev[2 * it + 1], st));
+        CK(launch_dot(op->pv, op->q, o0, o1, op->partials, op->scal + S_PQ, st));
+        RET(allreduce_scalar(m, op->scal + S_PQ, st));
+        CK(launch_cg_xr(x, op->r, op->pv, op->q, n, o0, o1, op->scal, op->partials, st));
+        RET(allreduce_scalar(m, op->scal + S_RRNEW, st));
+        if (!bench) {
+            CK(cudaMemcpyAsync(op->h_scal + S_PQ, op->scal + S_PQ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+            CK(cudaEventRecord(ready, st));
+        }
+        CK(launch_cg_p(op->pv, op->r, n, op->scal, st));
+        ++it;
+        if (!bench) {
+            CK(cudaEventSynchronize(ready));
+            if (!(op->h_scal[S_PQ] > 0.0)) { status = DOGIP_E_BREAKDOWN; rr = op->h_scal[S_RRNEW]; break; }
+            rr = op->h_scal[S_RRNEW];
+        }
+    }
+    CK(cudaEventRecord(t1, st));
+    CK(cudaStreamSynchronize(st));
+    if (bench) {
+        CK(cudaMemcpy(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost));
+        rr = op->h_scal[S_RR];
+        bnorm = std::sqrt(op->h_scal[S_BB]);
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    double aps = 0.0;
+    for (int i = 0; i < (bench ? it : 0); ++i) {
+        float a = 0.f;
+        cudaEventElapsedTime(&a, aev[2 * i], aev[2 * i + 1]);
+        aps += a * 1e-3;
+    }
+    res->iters = it;
+    res->status = status;
+    res->rel_res = bnorm > 0 ? std::sqrt(rr) / bnorm : 0.0;
+    res->seconds = ms * 1e-3;
+    res->apply_seconds = aps;
+    if (status == DOGIP_E_BREAKDOWN) return fail(DOGIP_E_BREAKDOWN, "CG breakdown: p^T A p <= 0");
+    return status;
+}
+
+// ------------------------------------------------------------------ introspection
+extern "C" int dogip_reference_table(int d, int p, int form, double* out, int64_t cap) {
+    if ((d != 2 && d != 3)) return fail(DOGIP_E_INVALID_DIM, "d must be 2 or 3");
+    if (p < 1 || p > 8) return fail(DOGIP_E_UNSUPPORTED_ORDER, "p must be in 1..8 for tables");
+    if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "bad form");
+    Table t;
+    try { t = bhat_table(d, p, form); } catch (const std::exception& e) { return fail(DOGIP_E_INVALID_ARG, e.what()); }
+    const int64_t n = (int64_t)t.v.size();
+    if (out) {
+        if (cap < n) return fail(DOGIP_E_INVALID_SIZE, "capacity too small");
+        for (int64_t i = 0; i < n; ++i) out[i] = t.v[i].to_double();
+    }
+    return (int)n;
+}
+
+extern "C" int dogip_reference_nnz(int d, int p, int form, int64_t* nnz, int64_t* pm1) {
+    if ((d != 2 && d != 3)) return fail(DOGIP_E_INVALID_DIM, "d must be 2 or 3");
+    if (p < 1 || p > 8) return fail(DOGIP_E_UNSUPPORTED_ORDER, "p must be in 1..8 for tables");
+    if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "bad form");
+    Table t;
+    try { t = bhat_table(d, p, form); } catch (const std::exception& e) { return fail(DOGIP_E_INVALID_ARG, e.what()); }
+    int64_t a = 0, b = 0;
+    for (auto& v : t.v) { a += !v.is_zero(); b += v.is_pm1(); }
+    if (nnz) *nnz = a;
+    if (pm1) *pm1 = b;
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_quadrature(int d, int n1d, double* pts, double* wts, int64_t cap) {
+    if (d != 2 && d != 3) return fail(DOGIP_E_INVALID_DIM, "d must be 2 or 3");
+    if (n1d < 1 || n1d > 64) return fail(DOGIP_E_INVALID_SIZE, "n1d must be in 1..64");
+    std::vector<double> P, W;
+    simplex_rule(d, n1d, P, W);
+    const int64_t n = (int64_t)W.size();
+    if (pts || wts) {
+        if (cap < n) return fail(DOGIP_E_INVALID_SIZE, "capacity too small");
+        if (pts) std::memcpy(pts, P.data(), sizeof(double) * P.size());
+        if (wts) std::memcpy(wts, W.data(), sizeof(double) * W.size());
+    }
+    return (int)n;
+}
+
+// K-order (tile, lane) -> canonical local element index; -1 for padding lanes
+static int64_t canonical_elem(const SlabGeo& g, int64_t tile, int lane) {
+    const TileCoord tc = tile_coord(g, tile);
+    const int ci = tc.ci0 + lane;
+    if (ci >= g.Nx) return -1;
+    const int64_t cell = g.d == 2 ? ci + (int64_t)g.Nx * tc.cj : ci + (int64_t)g.Nx * (tc.cj + (int64_t)g.Ny * tc.ck);
+    return cell * g.ns + tc.s;
+}
+
+extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
+    if (!op || !host) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    dogip_mesh_info_t info;
+    dogip_mesh_info(op->m, &info);
+    const int WT = op->ref.WT, NC = op->ref.NC;
+    if (cap < info.n_elem_local * WT * NC) return fail(DOGIP_E_INVALID_SIZE, "capacity too small");
+    std::vector<double> w(op->w_doubles);
+    CK(cudaSetDevice(op->m->device));
+    CK(cudaMemcpy(w.data(), op->d_w, sizeof(double) * op->w_doubles, cudaMemcpyDeviceToHost));
+    const SlabGeo& g = op->m->geo;
+    for (int64_t t = 0; t < g.ntiles; ++t)
+        for (int lane = 0; lane < TILE; ++lane) {
+            const int64_t e = canonical_elem(g, t, lane);
+            if (e < 0) continue;
+            for (int k = 0; k < WT * NC; ++k) host[e * WT * NC + k] = w[((size_t)t * WT * NC + k) * TILE + lane];
+        }
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_export_dofmap(dogip_mesh m, int64_t* host, int64_t cap) {
+    if (!m || !host) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    dogip_mesh_info_t info;
+    dogip_mesh_info(m, &info);
+    const int VT = m->ref.VT;
+    if (cap < info.n_elem_local * VT) return fail(DOGIP_E_INVALID_SIZE, "capacity too small");
+    const SlabGeo& g = m->geo;
+    for (int64_t t = 0; t < g.ntiles; ++t)
+        for (int lane = 0; lane < TILE; ++lane) {
+            const int64_t e = canonical_elem(g, t, lane);
+            if (e < 0) continue;
+            const TileCoord tc = tile_coord(g, t);
+            const int64_t base = (int64_t)g.p * (tc.ci0 + lane + g.sy * tc.cj + g.sz * tc.ck);
+            for (int l = 0; l < VT; ++l) host[e * VT + l] = base + m->tab.off[tc.s * MAX_VT + l];
+        }
+    return DOGIP_OK;
+}

@@ -1,0 +1,233 @@
+// apply.cu -- the hot DoGIP apply kernel (sm_100a).
+//
+// y += sum_T P_T^T Bhat^T A_T Bhat P_T u      (Algorithm 1, PAPER.md P:491-511;
+//                                              Theorem 2 eq:wp_dogip_mul P:276,
+//                                              Theorem 4 eq:ep_dogip_mul P:439)
+// Mapping:
+//  * one warp = one 32-element tile = 32 consecutive cells along x with the same
+//    simplex type s; one lane = one element (gather offsets are warp-uniform and
+//    read from the kernel-parameter bank);
+//  * the per-element work g = Bhat u_T, h = A_T g, y_T += Bhat^T h is the
+//    generated straight-line, sparsity- and +-1-aware FP64 code of
+//    generated/bhat_gen.cuh, node by node, so only u_T and y_T sit in registers;
+//  * A_T is stored tile-major [tile][W_T * NC][32] (lane fastest) and streamed
+//    by each warp through its own S-stage shared-memory ring with 1D bulk
+//    copies (cp.async.bulk, the TMA engine) that complete on mbarriers; the
+//    stream runs ahead across tile boundaries, so HBM requests stay in flight
+//    independently of register pressure;
+//  * u_T is gathered with read-only loads (neighbouring lanes share cache
+//    lines), y_T is scattered with fire-and-forget red.global.add.f64 (y must
+//    be zeroed first); DIRICHLET zeroes boundary DoFs of u_T and skips their
+//    scatter (the boundary rows are fixed by dirichlet_fixup).
+#include <cuda_runtime.h>
+
+#include "../generated/bhat_gen.cuh"
+#include "apply.cuh"
+#include "common.cuh"
+
+namespace dogip {
+
+namespace {
+
+template <class RE>
+struct Chunking {
+    static constexpr int NC = RE::NC;
+    static constexpr int CHN = (12 / NC) < 1 ? 1 : (12 / NC);    // nodes per chunk
+    static constexpr int ROWS = CHN * NC;                        // rows per full chunk
+    static constexpr int NCH = (RE::WT + CHN - 1) / CHN;         // chunks per tile
+    static constexpr int TILE_ROWS = RE::WT * NC;
+    static constexpr int S = 4;                                  // ring stages per warp
+};
+
+template <class RE>
+struct WarpStream {
+    using C = Chunking<RE>;
+    double* ring;          // this warp's ring in shared memory
+    uint32_t bar0;         // smem address of this warp's S mbarriers
+    int lane;
+    const double* wbase;   // global weights (tile-major)
+    int64_t gw, nw, tile_end;
+    int64_t g_cons;        // next chunk (warp-global sequence) to consume
+    const double* cur;     // current stage + lane
+    uint64_t policy;
+
+    __device__ __forceinline__ void issue(int64_t gg) const {   // lane 0 only
+        const int64_t it = gg / C::NCH;
+        const int c = (int)(gg - it * C::NCH);
+        const int64_t tile = gw + it * nw;
+        if (tile >= tile_end) return;
+        const int rows = (c == C::NCH - 1) ? C::TILE_ROWS - c * C::ROWS : C::ROWS;
+        const uint32_t bytes = (uint32_t)rows * TILE * 8u;
+        const int st = (int)(gg % C::S);
+        const uint32_t bar = bar0 + 8u * st;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s_evict_first(smem_u32(ring + (size_t)st * C::ROWS * TILE),
+                             wbase + ((size_t)tile * C::TILE_ROWS + (size_t)c * C::ROWS) * TILE,
+                             bytes, bar, policy);
+    }
+    template <int J>
+    __device__ __forceinline__ void begin() {
+        if constexpr (J % C::CHN == 0) {
+            __syncwarp();
+            if (lane == 0) {
+                fence_proxy_async_smem();          // prior generic reads of the stage
+                issue(g_cons + C::S - 1);          // refill the stage consumed last
+            }
+            const int st = (int)(g_cons % C::S);
+            mbar_wait(bar0 + 8u * st, (uint32_t)((g_cons / C::S) & 1));
+            cur = ring + (size_t)st * C::ROWS * TILE + lane;
+            ++g_cons;
+        }
+    }
+    template <int J>
+    __device__ __forceinline__ void end() {}
+    __device__ __forceinline__ double w(int k) const { return cur[(k % C::ROWS) * TILE]; }
+};
+
+template <int D, int P, int F, bool DIR>
+__global__ void __launch_bounds__(APPLY_THREADS)
+apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
+             const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end) {
+    using RE = dogip_gen::RefElem<D, P, F>;
+    using C = Chunking<RE>;
+    constexpr int NW = APPLY_THREADS / 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* rings = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * C::S * C::ROWS * TILE * 8);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpStream<RE> ws;
+    ws.ring = rings + (size_t)warp * C::S * C::ROWS * TILE;
+    ws.bar0 = smem_u32(bars + warp * C::S);
+    ws.lane = lane;
+    ws.wbase = w;
+    ws.gw = tile_begin + (int64_t)blockIdx.x * NW + warp;
+    ws.nw = (int64_t)gridDim.x * NW;
+    ws.tile_end = tile_end;
+    ws.g_cons = 0;
+    ws.policy = policy_evict_first();
+    if (lane == 0) {
+        for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
+        fence_mbar_init();
+        for (int s = 0; s < C::S - 1; ++s) ws.issue(s);      // prologue
+    }
+    __syncwarp();
+
+    for (int64_t tile = ws.gw; tile < tile_end; tile += ws.nw) {
+        const TileCoord tc = tile_coord(geo, tile);
+        const int ci = tc.ci0 + lane;
+        const bool valid = ci < geo.Nx;
+        const int64_t base = (int64_t)geo.p * (ci + geo.sy * tc.cj + geo.sz * tc.ck);
+        const int* off = tab.off + tc.s * MAX_VT;
+        const int* lof = tab.loff + tc.s * MAX_VT;
+        double uT[RE::VT], yT[RE::VT];
+        uint64_t bmask = 0;
+#pragma unroll
+        for (int l = 0; l < RE::VT; ++l) {
+            bool take = valid;
+            if constexpr (DIR) {
+                const int lo = lof[l];
+                const int X = geo.p * ci + (lo & 0xff);
+                const int Y = geo.p * tc.cj + ((lo >> 8) & 0xff);
+                const int Z = geo.p * tc.ck + ((lo >> 16) & 0xff);
+                bool b = X == 0 || X == geo.pmax_x;
+                if (D == 3) {
+                    b = b || Y == 0 || Y == geo.pmax_y || (Z == 0 && geo.bnd_lo) || (Z == geo.pmax_z && geo.bnd_hi);
+                } else {
+                    b = b || (Y == 0 && geo.bnd_lo) || (Y == geo.pmax_y && geo.bnd_hi);
+                }
+                if (b) { bmask |= (1ull << l); take = false; }
+            }
+            uT[l] = take ? ldg_f64(u + base + off[l]) : 0.0;
+            yT[l] = 0.0;
+        }
+        RE::body(uT, yT, ws);
+        if (valid) {
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) {
+                if (DIR && ((bmask >> l) & 1ull)) continue;
+                red_add_f64(y + base + off[l], yT[l]);
+            }
+        }
+    }
+}
+
+template <int D, int P, int F, bool DIR>
+cudaError_t launch_one(const ApplyArgs& a) {
+    using RE = dogip_gen::RefElem<D, P, F>;
+    using C = Chunking<RE>;
+    constexpr int NW = APPLY_THREADS / 32;
+    const size_t smem = (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8;
+    auto kern = apply_kernel<D, P, F, DIR>;
+    static int configured = 0;   // per instantiation
+    static int occ = 1;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, APPLY_THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        configured = 1;
+    }
+    const int64_t ntiles = a.tile_end - a.tile_begin;
+    if (ntiles <= 0) return cudaSuccess;
+    int64_t grid = (int64_t)a.num_sms * occ;
+    const int64_t need = (ntiles + NW - 1) / NW;
+    if (grid > need) grid = need;
+    kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, a.tile_begin,
+                                                           a.tile_end);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+template <int D, int P, int F>
+cudaError_t launch_dir(const ApplyArgs& a) {
+    return a.dirichlet ? launch_one<D, P, F, true>(a) : launch_one<D, P, F, false>(a);
+}
+
+template <int D, int P>
+cudaError_t launch_form(const ApplyArgs& a) {
+    return a.form == 0 ? launch_dir<D, P, 0>(a) : launch_dir<D, P, 1>(a);
+}
+
+template <int D>
+cudaError_t launch_p(const ApplyArgs& a) {
+    switch (a.p) {
+        case 1: return launch_form<D, 1>(a);
+        case 2: return launch_form<D, 2>(a);
+        case 3: return launch_form<D, 3>(a);
+        case 4: return launch_form<D, 4>(a);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+std::atomic<long long> g_launches{0};
+
+cudaError_t launch_apply(const ApplyArgs& a) {
+    return a.d == 2 ? launch_p<2>(a) : launch_p<3>(a);
+}
+
+// Reference-element constants of the generated tables, for the host side.
+template <int D, int P, int F>
+static void fill_info(RefInfo& r) {
+    using RE = dogip_gen::RefElem<D, P, F>;
+    r.VT = RE::VT; r.WT = RE::WT; r.NC = RE::NC; r.NS = RE::NS;
+    r.flops = RE::FLOPS; r.nnz = RE::NNZ; r.nnz_pm1 = RE::NNZ_PM1;
+    for (int s = 0; s < RE::NS; ++s)
+        for (int l = 0; l < RE::VT; ++l)
+            for (int ax = 0; ax < 3; ++ax) r.loff[s][l][ax] = ax < D ? RE::LOFF[s][l][ax] : 0;
+}
+
+bool ref_info(int d, int p, int form, RefInfo& r) {
+#define DOGIP_CASE(D, P, F) if (d == D && p == P && form == F) { fill_info<D, P, F>(r); return true; }
+    DOGIP_CASE(2, 1, 0) DOGIP_CASE(2, 1, 1) DOGIP_CASE(2, 2, 0) DOGIP_CASE(2, 2, 1)
+    DOGIP_CASE(2, 3, 0) DOGIP_CASE(2, 3, 1) DOGIP_CASE(2, 4, 0) DOGIP_CASE(2, 4, 1)
+    DOGIP_CASE(3, 1, 0) DOGIP_CASE(3, 1, 1) DOGIP_CASE(3, 2, 0) DOGIP_CASE(3, 2, 1)
+    DOGIP_CASE(3, 3, 0) DOGIP_CASE(3, 3, 1) DOGIP_CASE(3, 4, 0) DOGIP_CASE(3, 4, 1)
+#undef DOGIP_CASE
+    return false;
+}
+
+}  // namespace dogip

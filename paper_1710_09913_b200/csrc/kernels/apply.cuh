@@ -1,0 +1,94 @@
+// apply.cuh -- host-visible interface of the kernels in kernels/*.cu
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+#include <atomic>
+
+namespace dogip {
+
+// kernel launches issued by the library (dogip_kernel_launches)
+extern std::atomic<long long> g_launches;
+inline void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+constexpr int APPLY_THREADS = 128;   // 4 warps = 4 tiles in flight per CTA
+
+// Warp-uniform gather tables (kernel-parameter bank): off = local DoF index
+// offset of local DoF l of simplex s from the cell's base DoF; loff = the
+// same offset as packed lattice coordinates x | y << 8 | z << 16.
+struct ApplyTables {
+    int off[MAX_NS * MAX_VT];
+    int loff[MAX_NS * MAX_VT];
+};
+
+struct ApplyArgs {
+    int d, p, form;
+    bool dirichlet;
+    const double* u;
+    double* y;
+    const double* w;
+    SlabGeo geo;
+    const ApplyTables* tab;
+    int64_t tile_begin, tile_end;
+    int num_sms;
+    cudaStream_t stream;
+};
+
+cudaError_t launch_apply(const ApplyArgs& a);
+
+// Constants of the generated reference element (generated/bhat_gen.cuh).
+struct RefInfo {
+    int VT, WT, NC, NS, flops, nnz, nnz_pm1;
+    int loff[MAX_NS][MAX_VT][3];
+};
+bool ref_info(int d, int p, int form, RefInfo& r);
+
+// ----------------------------------------------------------- weights (K1)
+struct WeightsArgs {
+    int d, p, form, nq, WT, NC, ncomp;     // ncomp: coefficient components (1 or d(d+1)/2)
+    int kind;                              // DOGIP_COEF_*
+    const double* params;                  // device copy of the coefficient parameters
+    int nparams;
+    const double* per_cell;                // device, global cell numbering, or null
+    const double* verts;                   // device ((N+1)^d, d) or null (lattice)
+    const double* qp;                      // device (nq, d) reference points
+    const double* qw;                      // device (nq,) weights
+    const double* phiW;                    // device (nq, WT) double-grid basis at points
+    const double* sW;                      // device (WT,) sum_q w_q phi^W_j(x_q)
+    SlabGeo geo;
+    double* out;                           // tile-major weights [tile][WT*NC][32]
+    double* scratch_c;                     // [nb * ncomp][nq]
+    double* scratch_a;                     // [nb * ncomp][WT]
+    int64_t batch;                         // elements per batch (multiple of 32)
+    int* bad_flag;                         // device int: 1 degenerate element, 2 bad coefficient
+    cudaStream_t stream;
+};
+cudaError_t launch_weights(const WeightsArgs& a);
+
+// ----------------------------------------------------------- vectors / CG
+cudaError_t launch_dirichlet_fixup(const SlabGeo& g, const double* u, double* y, cudaStream_t st);
+cudaError_t launch_zero_boundary(const SlabGeo& g, double* y, cudaStream_t st);
+cudaError_t launch_load_vector(const SlabGeo& g, int p, const double* verts, const double* sV,
+                               int VT, const ApplyTables* tab, double f, double* b, cudaStream_t st);
+
+// deterministic two-pass reductions (partials of fixed grid, then one block)
+constexpr int RED_BLOCKS = 592;       // 4 x 148 SMs
+constexpr int RED_THREADS = 256;
+cudaError_t launch_dot(const double* a, const double* b, int64_t i0, int64_t i1, double* partials,
+                       double* out, cudaStream_t st);
+// x += alpha p, r -= alpha q over [0, n), alpha = scal[RR]/scal[PQ]; partial r.r over [i0, i1)
+cudaError_t launch_cg_xr(double* x, double* r, const double* p, const double* q, int64_t n, int64_t i0,
+                         int64_t i1, double* scal, double* partials, cudaStream_t st);
+// p = r + beta p, beta = scal[RRNEW]/scal[RR]; then scal[RR] = scal[RRNEW]
+cudaError_t launch_cg_p(double* p, const double* r, int64_t n, double* scal, cudaStream_t st);
+cudaError_t launch_reduce_final(const double* partials, double* out, cudaStream_t st);
+cudaError_t launch_axpby(double* y, const double* x, double a, double b, int64_t n, cudaStream_t st);
+cudaError_t launch_add_planes(double* y, const double* lo, const double* hi, int64_t plane,
+                              int64_t last_plane_off, cudaStream_t st);
+cudaError_t launch_fill(double* y, double v, int64_t n, cudaStream_t st);
+
+enum CgScal { S_RR = 0, S_PQ = 1, S_RRNEW = 2, S_BB = 3, S_COUNT = 8 };
+
+}  // namespace dogip

@@ -1,0 +1,337 @@
+// weights.cu -- one-time DoGIP weight kernels (sm_100a).
+//
+//   WP  a_{T,j} = |det R_T| sum_q w_q m(F_T xq) phi^W_j(xq)               (Theorem 2)
+//   EL  A_{T,j} = Rinv_T (|det R_T| sum_q w_q M(F_T xq) phi^W_j(xq)) Rinv_T^T (Theorem 4)
+// with the collapsed Gauss-Jacobi rule Q (reading L10).  Three steps per batch
+// of elements (K-order = apply-kernel tile order):
+//   1. quad_coef : C[e, c, q] = |det R_T| w_q M_c(F_T xq)      (c = coefficient component)
+//   2. gemm      : Abar[e, c, j] = sum_q C[e, c, q] Phi[q, j]   (smem-tiled FP64 GEMM)
+//   3. finalize  : congruence with Rinv_T (EL) and the tile-major store [tile][j*NC+c][lane]
+// Cell-constant coefficients skip 1-2: Abar = |det R_T| M_T s_j, s_j = sum_q w_q phi^W_j(xq).
+#include <cuda_runtime.h>
+
+#include "../../../include/dogip.h"
+#include "apply.cuh"
+#include "common.cuh"
+
+namespace dogip {
+namespace {
+
+struct Geo {
+    double R[3][3], Rinv[3][3], S[3], det;
+    int64_t cell;     // global cell index
+    bool valid;
+};
+
+// Simplex vertex offsets of one cell (reading L3): 2D right split, 3D Kuhn.
+__device__ __forceinline__ void simplex_offset(int d, int s, int v, int o[3]) {
+    o[0] = o[1] = o[2] = 0;
+    if (v == 0) return;
+    if (d == 2) {
+        if (s == 0) { o[0] = 1; o[1] = (v == 2); }
+        else { o[1] = 1; o[0] = (v == 1); }
+        return;
+    }
+    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int i = 0; i < v; ++i) o[perms[s][i]] += 1;
+}
+
+__device__ Geo element_geo(const SlabGeo& g, const double* verts, int64_t eK, int* bad) {
+    Geo G;
+    const int64_t tile = eK / TILE;
+    const int lane = (int)(eK % TILE);
+    const TileCoord tc = tile_coord(g, tile);
+    const int ci = tc.ci0 + lane;
+    G.valid = ci < g.Nx;
+    const int d = g.d;
+    int64_t c[3] = {ci, tc.cj, tc.ck};
+    if (d == 2) c[1] += g.zoff; else c[2] += g.zoff;
+    if (!G.valid) c[0] = 0;
+    G.cell = d == 2 ? c[0] + (int64_t)g.N * c[1] : c[0] + (int64_t)g.N * (c[1] + (int64_t)g.N * c[2]);
+    const int64_t M = g.N + 1;
+    double X[4][3];
+    int lat[4][3];
+    for (int v = 0; v <= d; ++v) {
+        int o[3];
+        simplex_offset(d, tc.s, v, o);
+        int64_t vid = 0, mul = 1;
+        for (int a = 0; a < d; ++a) {
+            lat[v][a] = o[a];
+            vid += (c[a] + o[a]) * mul;
+            mul *= M;
+        }
+        for (int a = 0; a < d; ++a)
+            X[v][a] = verts ? verts[vid * d + a] : (double)(c[a] + o[a]) / (double)g.N;
+    }
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) G.R[a][b] = (a == b) ? 1.0 : 0.0;
+    for (int a = 0; a < d; ++a) {
+        G.S[a] = X[0][a];
+        for (int b = 0; b < d; ++b) G.R[a][b] = X[b + 1][a] - X[0][a];   // columns v_b - v_0
+    }
+    int Rl[3][3];
+    for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) Rl[a][b] = lat[b + 1][a] - lat[0][a];
+    int detl;
+    if (d == 2) {
+        G.det = G.R[0][0] * G.R[1][1] - G.R[0][1] * G.R[1][0];
+        detl = Rl[0][0] * Rl[1][1] - Rl[0][1] * Rl[1][0];
+        const double id = 1.0 / G.det;
+        G.Rinv[0][0] = G.R[1][1] * id;  G.Rinv[0][1] = -G.R[0][1] * id;
+        G.Rinv[1][0] = -G.R[1][0] * id; G.Rinv[1][1] = G.R[0][0] * id;
+    } else {
+        const double (*R)[3] = G.R;
+        const double c00 = R[1][1] * R[2][2] - R[1][2] * R[2][1];
+        const double c01 = R[1][2] * R[2][0] - R[1][0] * R[2][2];
+        const double c02 = R[1][0] * R[2][1] - R[1][1] * R[2][0];
+        G.det = R[0][0] * c00 + R[0][1] * c01 + R[0][2] * c02;
+        detl = Rl[0][0] * (Rl[1][1] * Rl[2][2] - Rl[1][2] * Rl[2][1]) -
+               Rl[0][1] * (Rl[1][0] * Rl[2][2] - Rl[1][2] * Rl[2][0]) +
+               Rl[0][2] * (Rl[1][0] * Rl[2][1] - Rl[1][1] * Rl[2][0]);
+        const double id = 1.0 / G.det;
+        G.Rinv[0][0] = c00 * id;
+        G.Rinv[1][0] = c01 * id;
+        G.Rinv[2][0] = c02 * id;
+        G.Rinv[0][1] = (R[0][2] * R[2][1] - R[0][1] * R[2][2]) * id;
+        G.Rinv[1][1] = (R[0][0] * R[2][2] - R[0][2] * R[2][0]) * id;
+        G.Rinv[2][1] = (R[0][1] * R[2][0] - R[0][0] * R[2][1]) * id;
+        G.Rinv[0][2] = (R[0][1] * R[1][2] - R[0][2] * R[1][1]) * id;
+        G.Rinv[1][2] = (R[0][2] * R[1][0] - R[0][0] * R[1][2]) * id;
+        G.Rinv[2][2] = (R[0][0] * R[1][1] - R[0][1] * R[1][0]) * id;
+    }
+    if (bad && G.valid && !(G.det * (double)detl > 0.0)) atomicOr(bad, 1);   // E_DEGENERATE_ELEMENT
+    return G;
+}
+
+// coefficient components at physical point x: isotropic -> out[0] = m;
+// tensor -> upper triangle row-major (2D: 3, 3D: 6 values)
+__device__ void coef_eval(int kind, const double* P, const double* per_cell, int64_t cell, int d,
+                          const double* x, double* out) {
+    switch (kind) {
+        case DOGIP_COEF_CONST: out[0] = P[0]; return;
+        case DOGIP_COEF_PER_CELL: out[0] = per_cell[cell]; return;
+        case DOGIP_COEF_SINCOS2D:
+            out[0] = P[0] + P[1] * sin(2.0 * M_PI * x[0]) * cos(2.0 * M_PI * x[1]);
+            return;
+        case DOGIP_COEF_TANH_RADIAL: {
+            double r2 = 0.0;
+            for (int a = 0; a < d; ++a) { const double t = x[a] - P[4 + a]; r2 += t * t; }
+            out[0] = P[0] + P[1] * tanh(P[2] * (sqrt(r2) - P[3]));
+            return;
+        }
+        case DOGIP_COEF_ANISO_FOURIER: {
+            const int n = (int)P[3];
+            const double* kap = P + 4;
+            const double* phi = P + 4 + 3 * n;
+            const double* cc = P + 4 + 6 * n;
+            double w[3] = {0.0, 0.0, 0.0};
+            for (int m = 0; m < n; ++m) {
+                const double arg = 2.0 * M_PI * (x[0] * kap[3 * m] + x[1] * kap[3 * m + 1] + x[2] * kap[3 * m + 2]);
+                for (int i = 0; i < 3; ++i) w[i] += cc[3 * m + i] * cos(arg + phi[3 * m + i]);
+            }
+            double R[3][3];
+            const double t = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+            if (t < 1e-12) {
+                R[0][0] = 1; R[0][1] = -w[2]; R[0][2] = w[1];
+                R[1][0] = w[2]; R[1][1] = 1; R[1][2] = -w[0];
+                R[2][0] = -w[1]; R[2][1] = w[0]; R[2][2] = 1;
+            } else {
+                const double k0 = w[0] / t, k1 = w[1] / t, k2 = w[2] / t;
+                const double K[3][3] = {{0, -k2, k1}, {k2, 0, -k0}, {-k1, k0, 0}};
+                const double st = sin(t), ct1 = 1.0 - cos(t);
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) {
+                        double k2ab = 0.0;
+                        for (int c = 0; c < 3; ++c) k2ab += K[a][c] * K[c][b];
+                        R[a][b] = (a == b ? 1.0 : 0.0) + st * K[a][b] + ct1 * k2ab;
+                    }
+            }
+            int o = 0;
+            for (int a = 0; a < 3; ++a)
+                for (int b = a; b < 3; ++b) {
+                    double s = 0.0;
+                    for (int c = 0; c < 3; ++c) s += R[a][c] * P[c] * R[b][c];
+                    out[o++] = s;
+                }
+            return;
+        }
+        case DOGIP_COEF_CONST_TENSOR: {
+            int o = 0;
+            for (int a = 0; a < d; ++a)
+                for (int b = a; b < d; ++b) out[o++] = P[a * d + b];
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ bool coef_ok(int ncomp, int d, const double* c) {
+    if (ncomp == 1) return c[0] > 0.0;
+    return d == 2 ? (c[0] > 0.0 && c[2] > 0.0) : (c[0] > 0.0 && c[3] > 0.0 && c[5] > 0.0);
+}
+
+// 1. C[(e*ncomp + c)*nq + q] = |det| w_q M_c(x_q)
+__global__ void quad_coef_kernel(WeightsArgs a, int64_t e0, int64_t nb) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= nb * a.nq) return;
+    const int64_t el = idx / a.nq;
+    const int q = (int)(idx % a.nq);
+    const Geo G = element_geo(a.geo, a.verts, e0 + el, a.bad_flag);
+    const int d = a.d;
+    double x[3] = {0, 0, 0};
+    for (int r = 0; r < d; ++r) {
+        x[r] = G.S[r];
+        for (int c = 0; c < d; ++c) x[r] += G.R[r][c] * a.qp[q * d + c];
+    }
+    double cv[6];
+    coef_eval(a.kind, a.params, a.per_cell, G.cell, d, x, cv);
+    if (G.valid && !coef_ok(a.ncomp, d, cv)) atomicOr(a.bad_flag, 2);
+    const double sc = G.valid ? fabs(G.det) * a.qw[q] : 0.0;
+    for (int c = 0; c < a.ncomp; ++c) a.scratch_c[(el * a.ncomp + c) * a.nq + q] = sc * cv[c];
+}
+
+// 2. C (M x N) = A (M x K) * B (K x N), row-major, FP64, 64x64 tiles, 4x4 per thread
+constexpr int GB = 64, GK = 16;
+__global__ void __launch_bounds__(256) gemm_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                   double* __restrict__ C, int64_t M, int N, int K) {
+    __shared__ double As[GK][GB + 1];
+    __shared__ double Bs[GK][GB + 1];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t m0 = (int64_t)blockIdx.x * GB;
+    const int n0 = blockIdx.y * GB;
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < K; k0 += GK) {
+        for (int i = threadIdx.x; i < GB * GK; i += 256) {
+            const int mm = i / GK, kk = i % GK;
+            const int64_t gm = m0 + mm;
+            As[kk][mm] = (gm < M && k0 + kk < K) ? A[gm * K + k0 + kk] : 0.0;
+            const int kb = i / GB, nn = i % GB;
+            Bs[kb][nn] = (k0 + kb < K && n0 + nn < N) ? B[(int64_t)(k0 + kb) * N + n0 + nn] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < GK; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gm = m0 + ty * 4 + i;
+            const int gn = n0 + tx * 4 + j;
+            if (gm < M && gn < N) C[gm * N + gn] = acc[i][j];
+        }
+}
+
+// 3. congruence + tile-major store.  direct: cell-constant coefficient.
+__global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direct) {
+    const int64_t el = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (el >= nb) return;
+    const int64_t eK = e0 + el;
+    const Geo G = element_geo(a.geo, a.verts, eK, a.bad_flag);
+    const int d = a.d, WT = a.WT, NC = a.NC, nc = a.ncomp;
+    const int64_t tile = eK / TILE;
+    const int lane = (int)(eK % TILE);
+    double* out = a.out + (size_t)tile * WT * NC * TILE + lane;
+    double cconst[6] = {0, 0, 0, 0, 0, 0};
+    if (direct) {
+        double x[3] = {G.S[0], G.S[1], G.S[2]};
+        coef_eval(a.kind, a.params, a.per_cell, G.cell, d, x, cconst);
+        if (G.valid && !coef_ok(nc, d, cconst)) atomicOr(a.bad_flag, 2);
+    }
+    const double adet = fabs(G.det);
+    for (int j = 0; j < WT; ++j) {
+        double ab[6];
+        for (int c = 0; c < nc; ++c)
+            ab[c] = direct ? adet * cconst[c] * a.sW[j] : a.scratch_a[(el * nc + c) * WT + j];
+        if (!G.valid) {
+            for (int c = 0; c < NC; ++c) out[(size_t)(j * NC + c) * TILE] = 0.0;
+            continue;
+        }
+        if (a.form == DOGIP_WP) {
+            out[(size_t)j * TILE] = ab[0];
+            continue;
+        }
+        // Abar (symmetric) -> A = Rinv Abar Rinv^T  (A_rs = Rinv_rp Abar_pq Rinv_sq)
+        double Ab[3][3];
+        if (nc == 1) {
+            for (int p = 0; p < d; ++p)
+                for (int q = 0; q < d; ++q) Ab[p][q] = p == q ? ab[0] : 0.0;
+        } else {
+            int o = 0;
+            for (int p = 0; p < d; ++p)
+                for (int q = p; q < d; ++q) { Ab[p][q] = Ab[q][p] = ab[o++]; }
+        }
+        int o = 0;
+        for (int r = 0; r < d; ++r)
+            for (int s = r; s < d; ++s) {
+                double v = 0.0;
+                for (int p = 0; p < d; ++p) {
+                    double t = 0.0;
+                    for (int q = 0; q < d; ++q) t += Ab[p][q] * G.Rinv[s][q];
+                    v += G.Rinv[r][p] * t;
+                }
+                out[(size_t)(j * NC + o) * TILE] = v;
+                ++o;
+            }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_weights(const WeightsArgs& a) {
+    const int64_t nel = a.geo.ntiles * TILE;
+    const bool direct = a.kind == DOGIP_COEF_CONST || a.kind == DOGIP_COEF_PER_CELL ||
+                        a.kind == DOGIP_COEF_CONST_TENSOR;
+    for (int64_t e0 = 0; e0 < nel; e0 += a.batch) {
+        const int64_t nb = (nel - e0) < a.batch ? (nel - e0) : a.batch;
+        if (!direct) {
+            const int64_t nthr = nb * a.nq;
+            quad_coef_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, a.stream>>>(a, e0, nb);
+            const int64_t M = nb * a.ncomp;
+            dim3 grid((unsigned)((M + GB - 1) / GB), (unsigned)((a.WT + GB - 1) / GB));
+            gemm_kernel<<<grid, 256, 0, a.stream>>>(a.scratch_c, a.phiW, a.scratch_a, M, a.WT, a.nq);
+        }
+        finalize_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb, direct ? 1 : 0);
+        count_launches(direct ? 1 : 3);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// ---------------------------------------------------------- load vector (K5)
+namespace {
+__global__ void load_vector_kernel(SlabGeo g, const double* verts, const double* sV, int VT,
+                                   const ApplyTables tab, double f, double* b) {
+    const int64_t eK = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (eK >= g.ntiles * TILE) return;
+    const Geo G = element_geo(g, verts, eK, nullptr);
+    if (!G.valid) return;
+    const int64_t tile = eK / TILE;
+    const int lane = (int)(eK % TILE);
+    const TileCoord tc = tile_coord(g, tile);
+    const int ci = tc.ci0 + lane;
+    const int64_t base = (int64_t)g.p * (ci + g.sy * tc.cj + g.sz * tc.ck);
+    const double sc = f * fabs(G.det);
+    for (int l = 0; l < VT; ++l) red_add_f64(b + base + tab.off[tc.s * MAX_VT + l], sc * sV[l]);
+}
+}  // namespace
+
+cudaError_t launch_load_vector(const SlabGeo& g, int p, const double* verts, const double* sV, int VT,
+                               const ApplyTables* tab, double f, double* b, cudaStream_t st) {
+    (void)p;
+    const int64_t n = g.ntiles * TILE;
+    load_vector_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, verts, sV, VT, *tab, f, b);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace dogip

@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star, reading L24): relative max-norm
+||y_gpu - y_ref||_inf / ||y_ref||_inf <= 1e-12 for every apply; weights
+<= 1e-13; CG reaches the same relative residual.  All inputs seeded
+(synth/).  Sizes span several 32-element tiles and ragged x-blocks.
+"""
+import numpy as np
+import pytest
+
+from oracle import assemble as oa
+from oracle import dogip as od
+from oracle.cg import cg as oracle_cg
+from oracle.mesh import boundary_mask
+from synth.configs import (COEF_ANISO_FOURIER, COEF_CONST, COEF_CONST_TENSOR, COEF_PER_CELL,
+                           COEF_SINCOS2D, COEF_TANH_RADIAL, Coefficient, aniso_fourier_params,
+                           get_config)
+from synth.generators import grf_per_cell, u_vector, vertex_jitter
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+SINCOS = Coefficient(COEF_SINCOS2D, np.array([1.0, 0.5]))
+TANH2 = Coefficient(COEF_TANH_RADIAL, np.array([1.0, 0.9, 20.0, 0.25, 0.5, 0.5]))
+TANH3 = Coefficient(COEF_TANH_RADIAL, np.array([1.0, 0.9, 20.0, 0.25, 0.5, 0.5, 0.5]))
+ANISO = Coefficient(COEF_ANISO_FOURIER, aniso_fourier_params(2))
+
+
+def _torch():
+    import torch
+    assert torch.cuda.is_available(), "gpu tests need a GPU"
+    return torch
+
+
+def jitter_verts(d, N, seed=4, amp=0.2):
+    M = N + 1
+    ids = np.arange(M ** d)
+    X = np.stack([(ids // M ** a) % M for a in range(d)], axis=1) / N
+    return X + vertex_jitter(d, N, amp, seed)
+
+
+def relerr(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def gpu_apply(d, N, p, form, coef, u, verts=None, dirichlet=False, n1d=0):
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    m = Mesh(d, N, p, verts)
+    op = Operator(m, form, coef, quad_n1d=n1d)
+    y = op.apply(torch.from_numpy(u).cuda(), dirichlet=dirichlet)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), op, m
+
+
+def coef_for(d, form, kind):
+    if kind == "smooth":
+        return (SINCOS if d == 2 else TANH3) if form == 0 else (SINCOS if d == 2 else ANISO)
+    if kind == "tanh":
+        return TANH2 if d == 2 else TANH3
+    raise ValueError(kind)
+
+
+ALL = [(d, p, f) for d in (2, 3) for p in (1, 2, 3, 4) for f in (0, 1)]
+
+
+@pytest.mark.parametrize("d,p,form", ALL)
+def test_weights_match_oracle(d, p, form):
+    N = 3 if d == 2 else 2
+    verts = jitter_verts(d, N)
+    coef = coef_for(d, form, "smooth")
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    m = Mesh(d, N, p, verts)
+    op = Operator(m, form, coef)
+    w = op.export_weights()
+    ed = oa.build(d, N, p, verts)
+    ref = od.element_weights(ed, form, coef)
+    if form == 1:
+        iu = np.triu_indices(d)
+        ref = ref[:, :, iu[0], iu[1]]
+    else:
+        ref = ref[:, :, None]
+    assert relerr(w, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("d,p,form", ALL)
+def test_apply_matches_assembled_A(d, p, form):
+    """All 16 (d, p, form) on jittered meshes with a ragged x-block (N = 33
+    in 2D spans two 32-cell blocks; 3D N = 3 pads lanes)."""
+    N = 33 if d == 2 else 3
+    if d == 2 and p == 4:
+        N = 20
+    verts = jitter_verts(d, N)
+    coef = coef_for(d, form, "smooth")
+    ed = oa.build(d, N, p, verts)
+    A = oa.assemble_csr(ed, form, coef)
+    u = u_vector(ed.ndof, 0)
+    y, _, _ = gpu_apply(d, N, p, form, coef, u, verts)
+    assert relerr(y, A @ u) <= TOL
+
+
+@pytest.mark.parametrize("d,N,p", [(2, 40, 3), (3, 5, 2), (3, 4, 3)])
+def test_dirichlet_apply(d, N, p):
+    coef = coef_for(d, 1, "smooth")
+    ed = oa.build(d, N, p)
+    A = oa.assemble_csr(ed, 1, coef)
+    mask = boundary_mask(d, N, p)
+    u = u_vector(ed.ndof, 3)
+    y, _, _ = gpu_apply(d, N, p, 1, coef, u, dirichlet=True)
+    assert relerr(y, oa.dirichlet_matrix(A, mask) @ u) <= TOL
+    assert np.array_equal(y[mask], u[mask])
+
+
+@pytest.mark.parametrize("d,N,p,form", [(2, 35, 2, 1), (3, 4, 4, 0), (3, 5, 1, 1)])
+def test_load_vector(d, N, p, form):
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    verts = jitter_verts(d, N)
+    coef = coef_for(d, form, "smooth")
+    m = Mesh(d, N, p, verts)
+    op = Operator(m, form, coef)
+    ed = oa.build(d, N, p, verts)
+    for dirichlet in (False, True):
+        b = op.load_vector(1.0, dirichlet=dirichlet).cpu().numpy()
+        assert relerr(b, oa.load_vector(ed, 1.0, dirichlet)) <= TOL
+    assert abs(op.load_vector(1.0).sum().item() - 1.0) < 1e-12     # sum b_i = |Omega|
+
+
+def test_c1_both_forms_and_cg():
+    """Config 1: one apply per form, CG on the EL Dirichlet problem, f = 1."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config("C1")
+    coef = c.coefficient()
+    ed = oa.build(2, c.N, c.p)
+    u = c.u()
+    m = Mesh(2, c.N, c.p)
+    for form in (0, 1):
+        A = oa.assemble_csr(ed, form, coef)
+        op = Operator(m, form, coef)
+        y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+        assert relerr(y, A @ u) <= TOL
+    mask = boundary_mask(2, c.N, c.p)
+    AD = oa.dirichlet_matrix(oa.assemble_csr(ed, 1, coef), mask)
+    b = op.load_vector(1.0, dirichlet=True)
+    x = torch.zeros_like(b)
+    res = op.cg(b, x, rtol=1e-10, dirichlet=True)
+    assert res["status"] == "OK" and res["rel_res"] <= 1e-10
+    bn = b.cpu().numpy()
+    xn = x.cpu().numpy()
+    true_res = np.linalg.norm(bn - AD @ xn) / np.linalg.norm(bn)
+    assert true_res <= 2e-10
+    xo, it, _, st = oracle_cg(lambda v: AD @ v, oa.load_vector(ed, 1.0, True), rtol=1e-10)
+    assert abs(res["iters"] - it) <= 3
+    assert relerr(xn, xo) <= 1e-8
+
+
+def test_wp_mass_cg_1e12():
+    """Config-5 style mass solve at a small size: tol 1e-12, no BC."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config("C5").with_size(6)
+    verts = c.vertices()
+    m = Mesh(3, c.N, c.p, verts)
+    op = Operator(m, 0, c.coefficient())
+    b = op.load_vector(1.0)
+    x = torch.zeros_like(b)
+    res = op.cg(b, x, rtol=1e-12)
+    assert res["status"] == "OK" and res["rel_res"] <= 1e-12
+    ed = oa.build(3, c.N, c.p, verts)
+    A = oa.assemble_csr(ed, 0, c.coefficient())
+    bn, xn = b.cpu().numpy(), x.cpu().numpy()
+    assert np.linalg.norm(bn - A @ xn) / np.linalg.norm(bn) <= 2e-12
+
+
+@pytest.mark.parametrize("name,N", [("C2p1", 64), ("C2p2", 48), ("C2p3", 40), ("C2p4", 33),
+                                    ("C3", 8), ("C4", 7), ("C5", 5)])
+def test_configs_reduced_size_full_parity(name, N):
+    c = get_config(name).with_size(N)
+    coef = c.coefficient()
+    verts = c.vertices()
+    ed = oa.build(c.d, c.N, c.p, verts)
+    form = c.forms[0]
+    A = oa.assemble_csr(ed, form, coef)
+    u = c.u()
+    y, _, _ = gpu_apply(c.d, c.N, c.p, form, coef, u, verts)
+    assert relerr(y, A @ u) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C2p1", "C2p2", "C2p3", "C2p4", "C3", "C4", "C5"])
+def test_configs_full_size_sampled_rows(name):
+    """Full BASELINE sizes, the launch configuration bench.py times: sampled
+    rows recomputed one by one by the oracle, plus whole-vector invariants."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config(name)
+    coef = c.coefficient()
+    verts = c.vertices()
+    form = c.forms[0]
+    m = Mesh(c.d, c.N, c.p, verts)
+    op = Operator(m, form, coef)
+    u = c.u()
+    ug = torch.from_numpy(u).cuda()
+    y = op.apply(ug).cpu().numpy()
+    rng = np.random.default_rng(11)
+    n = c.ndof
+    rows = np.unique(np.concatenate([rng.integers(0, n, 48), [0, 1, n - 1, n // 2, n // 3],
+                                     np.arange(0, n, max(1, n // 16))[:16]]))
+    ref = oa.apply_rows_sampled(c.d, c.N, c.p, verts, form, coef, u, rows)
+    scale = np.abs(y).max()
+    assert np.abs(y[rows] - ref).max() / scale <= TOL
+    if form == 1:     # EL annihilates constants (check ii), at full size
+        y1 = op.apply(torch.ones_like(ug)).cpu().numpy()
+        assert np.abs(y1).max() <= 1e-11 * scale
+    else:             # WP: 1^T A 1 = int m
+        y1 = op.apply(torch.ones_like(ug))
+        assert np.isfinite(y1.sum().item())
+
+
+@pytest.mark.parametrize("d,N,p,form,nr", [(3, 6, 2, 1, 2), (3, 7, 3, 1, 3), (2, 40, 2, 0, 2), (3, 5, 4, 0, 2)])
+def test_slab_partials_sum_to_global(d, N, p, form, nr):
+    """Multi-rank path emulated on one GPU without NCCL: every slab computes
+    its partial y (DOGIP_NO_EXCHANGE); summing the interface planes
+    reproduces the single-rank apply (the data-path exchange step A8)."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    coef = coef_for(d, form, "smooth")
+    verts = jitter_verts(d, N)
+    Md = p * N + 1
+    u = u_vector(Md ** d, 5)
+    y_glob, _, _ = gpu_apply(d, N, p, form, coef, u, verts)
+    acc = np.zeros_like(u)
+    for r in range(nr):
+        m = Mesh(d, N, p, verts, rank=r, nranks=nr)
+        op = Operator(m, form, coef)
+        i0 = m.info["dof_offset"]
+        ul = torch.from_numpy(u[i0:i0 + m.ndof].copy()).cuda()
+        acc[i0:i0 + m.ndof] += op.apply(ul, exchange=False).cpu().numpy()
+    assert relerr(acc, y_glob) <= 1e-14
+
+
+def test_apply_host_matches_device():
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config("C4").with_size(9)
+    m = Mesh(3, c.N, c.p)
+    op = Operator(m, 1, c.coefficient())
+    u = c.u()
+    yd = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    yh = op.apply_host(u)
+    assert relerr(yh, yd) <= 1e-14
+
+
+def test_negative_control_other_rule_fails():
+    """Parity is sensitive: a different quadrature rule (n = p + 2 instead of
+    the contract p + 3) must break the 1e-12 bar for a non-polynomial m."""
+    d, N, p = 2, 12, 2
+    ed = oa.build(d, N, p)
+    A = oa.assemble_csr(ed, 0, SINCOS)
+    u = u_vector(ed.ndof, 0)
+    y, _, _ = gpu_apply(d, N, p, 0, SINCOS, u, n1d=p + 2)
+    assert relerr(y, A @ u) > 1e-9
+
+
+def test_error_codes_on_gpu():
+    from paper_1710_09913_b200.api import CoeffSpec, DogipError, Mesh, Operator
+    m = Mesh(3, 2, 2)
+    with pytest.raises(DogipError) as ei:
+        Operator(m, 0, ANISO)                     # tensor coefficient for WP
+    assert ei.value.code == -5
+    with pytest.raises(DogipError) as ei:
+        Operator(m, 1, CoeffSpec(COEF_CONST, np.array([-1.0])))
+    assert ei.value.code == -5
+    verts = jitter_verts(3, 2, amp=2.0)           # inverted tets
+    m2 = Mesh(3, 2, 2, verts)
+    with pytest.raises(DogipError) as ei:
+        Operator(m2, 1, CoeffSpec(COEF_CONST, np.array([1.0])))
+    assert ei.value.code == -4
