@@ -64,6 +64,12 @@ extern "C" {
                                         params = {e_1,e_2,e_3, n, kappa(n*3), phi(n*3), c(n*3)} */
 #define DOGIP_COEF_CONST_TENSOR   5  /* M = params[0..d*d) row-major, symmetric (EL only)   */
 
+/* ---- weight storage (dogip_weights_ex) ---------------------------------- */
+#define DOGIP_STORE_FULL  0  /* WP: a_{T,j}; EL: symmetric A_{T,j} (d(d+1)/2 per node)    */
+#define DOGIP_STORE_ISO   1  /* EL with isotropic M = m I (Corollary, element-wise):
+                                A_{T,j} = a_{T,j} G_T, a_{T,j} = int_T m phi^W_j, G_T = Rinv Rinv^T;
+                                stores W_T + d(d+1)/2 doubles per element instead of W_T d(d+1)/2 */
+
 /* ---- status codes ------------------------------------------------------- */
 #define DOGIP_OK                     0
 #define DOGIP_NOT_CONVERGED          1  /* CG hit maxit (x holds the last iterate)           */
@@ -119,6 +125,9 @@ typedef struct {
     int     W_T;                /* C(2p+d, d) (WP) or C(2p-2+d, d) (EL) double-grid nodes    */
     int     n_c;                /* stored weights per node: 1 (WP), d(d+1)/2 (EL, reading L11)*/
     int     quad_n1d;           /* points per direction of the weight rule (reading L10)     */
+    int     storage;            /* DOGIP_STORE_*                                             */
+    int     stream_doubles_per_elem; /* doubles the apply streams per element               */
+    int     flops_per_elem;     /* fp64 flops of the generated element body                  */
     int64_t n_tiles;            /* 32-element tiles of the apply kernel                      */
     int64_t weight_bytes;       /* device bytes of the streamed weights (incl. tile padding) */
     double  weights_ms;         /* device time of the one-time weights kernels               */
@@ -177,6 +186,12 @@ int dogip_slab_range(int64_t N, int rank, int nranks, int64_t* z0, int64_t* z1);
  */
 int dogip_weights(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_n1d,
                   void* stream, dogip_op* out);
+
+/* dogip_weights with an explicit storage variant (DOGIP_STORE_*).  DOGIP_STORE_ISO
+ * needs form = DOGIP_EL (else E_INVALID_ARG) and an isotropic coefficient kind
+ * (else E_BAD_COEFF); the apply result is the same operator up to rounding. */
+int dogip_weights_ex(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_n1d, int storage,
+                     void* stream, dogip_op* out);
 
 int dogip_op_info(dogip_op op, dogip_op_info_t* out);
 

@@ -12,6 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdogip.so")
 
 DOGIP_WP, DOGIP_EL = 0, 1
+DOGIP_STORE_FULL, DOGIP_STORE_ISO = 0, 1
 DOGIP_DIRICHLET_ZERO, DOGIP_NO_EXCHANGE, DOGIP_CG_RESUME = 1, 2, 4
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "E_INVALID_DIM", -2: "E_INVALID_SIZE",
           -3: "E_UNSUPPORTED_ORDER", -4: "E_DEGENERATE_ELEMENT", -5: "E_BAD_COEFF", -6: "E_OOM",
@@ -35,7 +36,8 @@ class Coeff(C.Structure):
 
 class OpInfo(C.Structure):
     _fields_ = [("form", C.c_int), ("d", C.c_int), ("p", C.c_int), ("V_T", C.c_int), ("W_T", C.c_int),
-                ("n_c", C.c_int), ("quad_n1d", C.c_int), ("n_tiles", C.c_int64),
+                ("n_c", C.c_int), ("quad_n1d", C.c_int), ("storage", C.c_int),
+                ("stream_doubles_per_elem", C.c_int), ("flops_per_elem", C.c_int), ("n_tiles", C.c_int64),
                 ("weight_bytes", C.c_int64), ("weights_ms", C.c_double)]
 
 
@@ -55,6 +57,8 @@ SIGNATURES = [
     ("dogip_mesh_info", C.c_int, [C.c_void_p, C.POINTER(MeshInfo)]),
     ("dogip_weights", C.c_int, [C.c_void_p, C.c_int, C.POINTER(Coeff), C.c_int, C.c_void_p,
                                 C.POINTER(C.c_void_p)]),
+    ("dogip_weights_ex", C.c_int, [C.c_void_p, C.c_int, C.POINTER(Coeff), C.c_int, C.c_int, C.c_void_p,
+                                   C.POINTER(C.c_void_p)]),
     ("dogip_op_info", C.c_int, [C.c_void_p, C.POINTER(OpInfo)]),
     ("dogip_apply", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]),
     ("dogip_apply_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint, C.c_void_p]),
@@ -86,10 +90,11 @@ def load() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+    path = os.environ.get("DOGIP_LIB", LIB_PATH)     # A/B experiments: libdogip_<variant>.so
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(there is no CPU fallback)")
-    lib = C.CDLL(LIB_PATH)
+    lib = C.CDLL(path)
     for name, res, args in SIGNATURES:
         f = getattr(lib, name)
         f.restype = res

@@ -134,15 +134,15 @@ class Mesh:
 class Operator:
     """A^DoGIP of one form on a mesh (dogip_weights) + apply / load vector / CG."""
 
-    def __init__(self, mesh: Mesh, form: int, coeff, quad_n1d: int = 0, stream=None):
+    def __init__(self, mesh: Mesh, form: int, coeff, quad_n1d: int = 0, stream=None, storage: int = 0):
         self.mesh = mesh
         self._lib = mesh._lib
         self.coeff = coeff if isinstance(coeff, CoeffSpec) else CoeffSpec.from_obj(coeff)
         cs = _lib.Coeff(self.coeff.kind, _dptr(self.coeff.params), self.coeff.params.size,
                         _dptr(self.coeff.per_cell))
         h = C.c_void_p()
-        check(self._lib.dogip_weights(mesh.handle, form, C.byref(cs), quad_n1d, C.c_void_p(_stream_ptr(stream)),
-                                      C.byref(h)))
+        check(self._lib.dogip_weights_ex(mesh.handle, form, C.byref(cs), quad_n1d, storage,
+                                         C.c_void_p(_stream_ptr(stream)), C.byref(h)))
         self.handle = h
         oi = _lib.OpInfo()
         check(self._lib.dogip_op_info(h, C.byref(oi)))

@@ -45,45 +45,59 @@ def _run(cmd):
     return r.stdout + r.stderr
 
 
-def generate(verbose=False):
+def generate(verbose=False, gen_out=GEN_OUT, gen_args=(), build_dir=BUILD):
     gen_src = os.path.join(CSRC, "gen", "gen_bhat.cpp")
-    gen_bin = os.path.join(BUILD, "gen_bhat")
+    gen_bin = os.path.join(build_dir, "gen_bhat")
     deps = [gen_src, os.path.join(CSRC, "host", "tables.hpp")]
-    if _mtime(GEN_OUT) >= max(_mtime(p) for p in deps):
+    if _mtime(gen_out) >= max(_mtime(p) for p in deps) and not gen_args:
         return
-    os.makedirs(BUILD, exist_ok=True)
-    os.makedirs(os.path.dirname(GEN_OUT), exist_ok=True)
+    os.makedirs(build_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(gen_out), exist_ok=True)
     _run(["g++", "-O2", "-std=c++17", "-o", gen_bin, gen_src])
-    _run([gen_bin, GEN_OUT])
+    _run([gen_bin, gen_out] + list(gen_args))
     if verbose:
         print("generated", GEN_OUT)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    generate(verbose)
-    os.makedirs(BUILD, exist_ok=True)
-    hdr_t = max(_mtime(h) for h in _headers())
+def build(verbose: bool = False, force: bool = False, variant: str = "", defines=(), gen_args=()) -> str:
+    """variant != "": an experimental A/B build into _build_<variant>/ and
+    libdogip_<variant>.so (load it with DOGIP_LIB=<path>)."""
+    build_dir = BUILD + (f"_{variant}" if variant else "")
+    lib = LIB if not variant else os.path.join(PKG, f"libdogip_{variant}.so")
+    gen_out = GEN_OUT if not variant else os.path.join(build_dir, "gen", "bhat_gen.cuh")
+    generate(verbose, gen_out, gen_args, build_dir)
+    os.makedirs(build_dir, exist_ok=True)
+    hdr_t = max(_mtime(h) for h in _headers() + [gen_out])
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                    "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+                    "-I", os.path.join(ROOT, "include"), "-I", CSRC] + [f"-D{d}" for d in defines]
+    if variant:
+        flags += ["-DDOGIP_GEN_HEADER=\"" + gen_out + "\""]
     jobs = []
     objs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace("/", "_") + ".o")
+        o = os.path.join(build_dir, src.replace("/", "_") + ".o")
         objs.append(o)
         if force or _mtime(o) < max(_mtime(s), hdr_t):
             jobs.append([NVCC] + flags + ["-c", s, "-o", o])
     if jobs:
         with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
             logs = list(ex.map(_run, jobs))
-        with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
+        with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
             f.write("\n".join(logs))
-    if jobs or _mtime(LIB) < max(_mtime(o) for o in objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-ldl"])
+    if jobs or _mtime(lib) < max(_mtime(o) for o in objs):
+        _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-ldl"])
         if verbose:
-            print("linked", LIB)
-    return LIB
+            print("linked", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    ap.add_argument("--gen-arg", dest="gen_args", action="append", default=[])
+    a = ap.parse_args()
+    build(verbose=True, force=a.force, variant=a.variant, defines=a.defines, gen_args=a.gen_args)

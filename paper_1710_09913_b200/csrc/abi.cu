@@ -60,7 +60,7 @@ struct dogip_mesh_s {
 
 struct dogip_op_s {
     dogip_mesh_s* m = nullptr;
-    int form = 0, nq = 0;
+    int form = 0, nq = 0, store = 0;
     RefInfo ref{};
     double* d_w = nullptr;
     int64_t w_doubles = 0;
@@ -118,7 +118,7 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
     m->d = d; m->N = N; m->p = p; m->rank = rank; m->nranks = nranks; m->device = device;
     dogip_slab_range(N, rank, nranks, &m->z0, &m->z1);
     const int64_t L = m->z1 - m->z0, M = p * N + 1;
-    ref_info(d, p, 0, m->ref);
+    ref_info(d, p, 0, 0, m->ref);
     SlabGeo& g = m->geo;
     g.d = d; g.p = p; g.ns = d == 2 ? 2 : 6; g.N = (int)N;
     g.Nx = (int)N;
@@ -256,19 +256,31 @@ struct DevBufs {   // frees on scope exit
 
 extern "C" int dogip_weights(dogip_mesh m, int form, const dogip_coeff* coeff, int quad_n1d, void* stream,
                              dogip_op* out) {
+    return dogip_weights_ex(m, form, coeff, quad_n1d, DOGIP_STORE_FULL, stream, out);
+}
+
+extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff, int quad_n1d, int storage,
+                                void* stream, dogip_op* out) {
     if (!m || !out) return fail(DOGIP_E_INVALID_ARG, "null argument");
     *out = nullptr;
     if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
+    if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO)
+        return fail(DOGIP_E_INVALID_ARG, "unknown storage");
+    if (storage == DOGIP_STORE_ISO && form != DOGIP_EL)
+        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_ISO applies to the elliptic form only");
     if (m->device < 0) return fail(DOGIP_E_INVALID_ARG, "host-only mesh (device < 0) cannot hold an operator");
     int ncomp = 1;
     RET(check_coeff(m->d, form, coeff, ncomp));
+    if (storage == DOGIP_STORE_ISO && ncomp != 1)
+        return fail(DOGIP_E_BAD_COEFF, "DOGIP_STORE_ISO needs an isotropic coefficient (M = m I)");
     CK(cudaSetDevice(m->device));
     cudaStream_t st = (cudaStream_t)stream;
     const int d = m->d, p = m->p;
     auto* op = new dogip_op_s();
     op->m = m;
     op->form = form;
-    ref_info(d, p, form, op->ref);
+    op->store = storage;
+    ref_info(d, p, form, storage, op->ref);
     const int WT = op->ref.WT, NC = op->ref.NC, VT = op->ref.VT;
     const int n1d = quad_n1d > 0 ? quad_n1d : p + 3;
     std::vector<double> pts, wts;
@@ -289,7 +301,7 @@ extern "C" int dogip_weights(dogip_mesh m, int form, const dogip_coeff* coeff, i
         for (int q = 0; q < nq; ++q) s += (long double)wts[q] * phiV[(size_t)q * VT + l];
         sV[l] = (double)s;
     }
-    op->w_doubles = m->geo.ntiles * (int64_t)WT * NC * TILE;
+    op->w_doubles = m->geo.ntiles * (int64_t)op->ref.tile_rows * TILE;
     auto cleanup_fail = [&](int code, const std::string& msg) { dogip_op_destroy(op); return fail(code, msg); };
     if (cudaMalloc(&op->d_w, sizeof(double) * op->w_doubles) != cudaSuccess)
         return cleanup_fail(DOGIP_E_OOM, "weights allocation (" + std::to_string(op->w_doubles * 8) + " bytes)");
@@ -298,7 +310,8 @@ extern "C" int dogip_weights(dogip_mesh m, int form, const dogip_coeff* coeff, i
 
     DevBufs tmp;
     WeightsArgs a{};
-    a.d = d; a.p = p; a.form = form; a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
+    a.d = d; a.p = p; a.form = form; a.store = storage; a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
+    a.NG = op->ref.NG; a.tile_rows = op->ref.tile_rows;
     a.kind = coeff->kind;
     a.nparams = (int)coeff->nparams;
     a.geo = m->geo;
@@ -353,7 +366,11 @@ extern "C" int dogip_weights(dogip_mesh m, int form, const dogip_coeff* coeff, i
 extern "C" int dogip_op_info(dogip_op op, dogip_op_info_t* o) {
     if (!op || !o) return fail(DOGIP_E_INVALID_ARG, "null argument");
     o->form = op->form; o->d = op->m->d; o->p = op->m->p;
-    o->V_T = op->ref.VT; o->W_T = op->ref.WT; o->n_c = op->ref.NC;
+    o->V_T = op->ref.VT; o->W_T = op->ref.WT;
+    o->n_c = op->form == DOGIP_WP ? 1 : op->m->d * (op->m->d + 1) / 2;
+    o->storage = op->store;
+    o->stream_doubles_per_elem = op->ref.tile_rows;
+    o->flops_per_elem = op->ref.flops;
     o->quad_n1d = op->nq;
     o->n_tiles = op->m->geo.ntiles;
     o->weight_bytes = op->w_doubles * 8;
@@ -403,7 +420,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
     const SlabGeo& g = m->geo;
     CK(cudaMemsetAsync(y, 0, sizeof(double) * g.ndof, st));
     ApplyArgs a{};
-    a.d = m->d; a.p = m->p; a.form = op->form;
+    a.d = m->d; a.p = m->p; a.form = op->form; a.store = op->store;
     a.dirichlet = (flags & DOGIP_DIRICHLET_ZERO) != 0;
     a.u = u; a.y = y; a.w = op->d_w; a.geo = g; a.tab = &m->tab;
     a.num_sms = m->num_sms;
@@ -644,7 +661,8 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
     if (!op || !host) return fail(DOGIP_E_INVALID_ARG, "null argument");
     dogip_mesh_info_t info;
     dogip_mesh_info(op->m, &info);
-    const int WT = op->ref.WT, NC = op->ref.NC;
+    const int d = op->m->d, WT = op->ref.WT, TR = op->ref.tile_rows;
+    const int NC = op->form == DOGIP_WP ? 1 : d * (d + 1) / 2;
     if (cap < info.n_elem_local * WT * NC) return fail(DOGIP_E_INVALID_SIZE, "capacity too small");
     std::vector<double> w(op->w_doubles);
     CK(cudaSetDevice(op->m->device));
@@ -654,7 +672,11 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
         for (int lane = 0; lane < TILE; ++lane) {
             const int64_t e = canonical_elem(g, t, lane);
             if (e < 0) continue;
-            for (int k = 0; k < WT * NC; ++k) host[e * WT * NC + k] = w[((size_t)t * WT * NC + k) * TILE + lane];
+            auto at = [&](int row) { return w[((size_t)t * TR + row) * TILE + lane]; };
+            for (int j = 0; j < WT; ++j)
+                for (int c = 0; c < NC; ++c)
+                    host[(e * WT + j) * NC + c] =
+                        op->store == DOGIP_STORE_ISO ? at(op->ref.NG + j) * at(c) : at(j * NC + c);
         }
     return DOGIP_OK;
 }

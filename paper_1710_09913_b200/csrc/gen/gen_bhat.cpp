@@ -13,6 +13,8 @@
 // bracket each node so the kernel can pipeline the weight stream.
 //
 // Usage: gen_bhat <output.cuh>
+#include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -59,106 +61,157 @@ static int emit_combo(FILE* f, const char* indent, const std::string& dst, bool 
     return flops;
 }
 
+// One storage variant of one (d, p, form):
+//   STORE 0 (full)  rows per node NC = 1 (WP) or d(d+1)/2 (EL upper triangle of A_{T,j})
+//   STORE 1 (iso)   EL with isotropic M = m I (Corollary, element-wise):
+//                   A_{T,j} = a_{T,j} G_T, G_T = Rinv Rinv^T; NG = d(d+1)/2 leading
+//                   rows hold G_T, then one row a_{T,j} per node.
+// interpolated values per emission group (argv[2]); 1 = node by node, which measured
+// best on B200 (profiles/r01_ab_variants.log: grouping 12 values was neutral-to-worse)
+static int g_gmax_vals = 1;
+
+static void emit_variant(FILE* f, int d, int p, int form, int store) {
+    Table t = bhat_table(d, p, form);
+    const int VT = t.cols, WT = t.rows;
+    const int NSYM = d * (d + 1) / 2;
+    const int NC = (form == 0 || store == 1) ? 1 : NSYM;
+    const int NG = store == 1 ? NSYM : 0;
+    const int ROWS = 12;                                   // rows per streamed chunk (3 KB / warp)
+    const int TILE_ROWS = NG + WT * NC;
+    int nnz = 0, pm1 = 0;
+    for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
+    auto simp = cell_simplices(d);
+    auto A = multi_indices(d, p);
+    std::fprintf(f, "template <> struct RefElem<%d, %d, %d, %d> {\n", d, p, form, store);
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = %d, NG = %d, ROWS = %d, TILE_ROWS = %d, NS = %d;\n",
+                 VT, WT, NC, NG, ROWS, TILE_ROWS, (int)simp.size());
+    std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
+    std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
+    for (size_t s = 0; s < simp.size(); ++s) {
+        std::fprintf(f, "%s{", s ? ", " : "");
+        for (int l = 0; l < VT; ++l) {
+            std::fprintf(f, "%s{", l ? "," : "");
+            for (int ax = 0; ax < d; ++ax) {
+                int o = 0;
+                for (int i = 0; i <= d; ++i) o += A[l][i] * simp[s][i][ax];
+                std::fprintf(f, "%s%d", ax ? "," : "", o);
+            }
+            std::fprintf(f, "}");
+        }
+        std::fprintf(f, "}");
+    }
+    std::fprintf(f, "};\n");
+    // row of node j's first weight, and its chunk
+    auto row = [&](int j) { return NG + j * NC; };
+    auto chunk = [&](int j) { return row(j) / ROWS; };
+    std::fprintf(f, "    static __host__ __device__ constexpr int row_of(int j) { return %d + j * %d; }\n", NG, NC);
+    std::fprintf(f,
+        "    template <class Pol>\n"
+        "    static __device__ __forceinline__ void body(const double* __restrict__ u,\n"
+        "                                                double* __restrict__ y, Pol& pol) {\n");
+    int flops = 0;
+    int idx[3][3], c = 0;
+    for (int r = 0; r < d; ++r)
+        for (int s2 = r; s2 < d; ++s2) { idx[r][s2] = idx[s2][r] = c++; }
+    // Nodes are emitted in groups = the nodes whose weights share one streamed chunk:
+    // all interpolations of a group first (independent FMA chains -> ILP), then weight
+    // multiply + projection node by node.
+    if (store == 1) {   // G_T rows lead the first chunk: open it, keep G_T in registers
+        std::fprintf(f, "        pol.template begin<0>();\n");
+        for (int k = 0; k < NG; ++k) std::fprintf(f, "        const double G%d = pol.w(%d);\n", k, k);
+    }
+    for (int j0 = 0; j0 < WT;) {
+        // a group never spans a chunk and holds at most 12 interpolated values
+        const int gmax = std::max(1, g_gmax_vals / t.nblk);
+        int j1 = j0;
+        while (j1 < WT && chunk(j1) == chunk(j0) && j1 - j0 < gmax) ++j1;
+        std::fprintf(f, "        {\n");
+        for (int j = j0; j < j1; ++j)
+            if (!(store == 1 && j == 0)) std::fprintf(f, "          pol.template begin<%d>();\n", j);
+        for (int j = j0; j < j1; ++j)
+            for (int b = 0; b < t.nblk; ++b) {
+                std::vector<std::pair<int, Rat>> terms;
+                for (int l = 0; l < VT; ++l)
+                    if (!t.at(b, j, l).is_zero()) terms.push_back({l, t.at(b, j, l)});
+                flops += emit_combo(f, "          ", "g" + std::to_string(b) + "_" + std::to_string(j), true, terms, "u");
+            }
+        for (int j = j0; j < j1; ++j) {
+            const std::string sj = "_" + std::to_string(j);
+            if (form == 0) {
+                std::fprintf(f, "          const double h0%s = pol.w(%d) * g0%s;\n", sj.c_str(), row(j), sj.c_str());
+                flops += 1;
+            } else if (store == 0) {
+                for (int k = 0; k < NC; ++k)
+                    std::fprintf(f, "          const double a%d%s = pol.w(%d);\n", k, sj.c_str(), row(j) + k);
+                for (int r = 0; r < d; ++r) {
+                    std::string acc = "a" + std::to_string(idx[r][0]) + sj + " * g0" + sj;
+                    for (int s2 = 1; s2 < d; ++s2)
+                        acc = "__fma_rn(a" + std::to_string(idx[r][s2]) + sj + ", g" + std::to_string(s2) + sj + ", " + acc + ")";
+                    std::fprintf(f, "          const double h%d%s = %s;\n", r, sj.c_str(), acc.c_str());
+                    flops += 2 * d - 1;
+                }
+            } else {
+                std::fprintf(f, "          const double a%s = pol.w(%d);\n", sj.c_str(), row(j));
+                for (int s2 = 0; s2 < d; ++s2)
+                    std::fprintf(f, "          const double t%d%s = a%s * g%d%s;\n", s2, sj.c_str(), sj.c_str(), s2, sj.c_str());
+                flops += d;
+                for (int r = 0; r < d; ++r) {
+                    std::string acc = "G" + std::to_string(idx[r][0]) + " * t0" + sj;
+                    for (int s2 = 1; s2 < d; ++s2)
+                        acc = "__fma_rn(G" + std::to_string(idx[r][s2]) + ", t" + std::to_string(s2) + sj + ", " + acc + ")";
+                    std::fprintf(f, "          const double h%d%s = %s;\n", r, sj.c_str(), acc.c_str());
+                    flops += 2 * d - 1;
+                }
+            }
+            for (int l = 0; l < VT; ++l) {
+                std::string acc = "y[" + std::to_string(l) + "]";
+                bool any = false;
+                for (int b = 0; b < t.nblk; ++b) {
+                    Rat cv = t.at(b, j, l);
+                    if (cv.is_zero()) continue;
+                    any = true;
+                    std::string h = "h" + std::to_string(b) + sj;
+                    if (cv == Rat(1)) acc = "(" + acc + ") + " + h;
+                    else if (cv == Rat(-1)) acc = "(" + acc + ") - " + h;
+                    else { acc = "__fma_rn(" + lit(cv.to_double()) + ", " + h + ", " + acc + ")"; flops += 1; }
+                    flops += 1;
+                }
+                if (any) std::fprintf(f, "          y[%d] = %s;\n", l, acc.c_str());
+            }
+        }
+        for (int j = j0; j < j1; ++j) std::fprintf(f, "          pol.template end<%d>();\n", j);
+        std::fprintf(f, "        }\n");
+        j0 = j1;
+    }
+    std::fprintf(f, "    }\n");
+    std::fprintf(f, "    static constexpr int FLOPS = %d;\n", flops);
+    std::fprintf(f, "};\n\n");
+}
+
 int main(int argc, char** argv) {
-    if (argc < 2) { std::fprintf(stderr, "usage: gen_bhat out.cuh\n"); return 2; }
+    if (argc < 2) { std::fprintf(stderr, "usage: gen_bhat out.cuh [group_values]\n"); return 2; }
+    if (argc > 2) g_gmax_vals = std::atoi(argv[2]);
     FILE* f = std::fopen(argv[1], "w");
     if (!f) { std::perror("open"); return 1; }
     std::fprintf(f,
         "// AUTO-GENERATED by csrc/gen/gen_bhat.cpp from the exact tables of host/tables.hpp.\n"
-        "// Do not edit.  One specialisation of RefElem<D,P,FORM> per (d, p, form):\n"
-        "//   VT = C(p+d,d), WT = #double-grid nodes, NC = stored weights per node,\n"
+        "// Do not edit.  One specialisation RefElem<D,P,FORM,STORE> per (d, p, form, storage):\n"
+        "//   VT = C(p+d,d), WT = #double-grid nodes, NC = streamed rows per node,\n"
+        "//   NG = leading per-element rows (iso storage: G_T = Rinv Rinv^T upper triangle),\n"
+        "//   ROWS = rows per streamed chunk, TILE_ROWS = NG + WT*NC rows per 32-element tile,\n"
         "//   FLOPS = fp64 flops of body() per element (sparse, +-1 aware),\n"
         "//   NNZ / NNZ_PM1 = nnz Bhat / nnz_{+-1} Bhat (eq:comp_eff, PAPER.md P:548),\n"
         "//   LOFF[s][l][a] = DoF-lattice offset (axis a) of local DoF l of simplex s\n"
         "//                   inside its cell, in units of the DoF lattice.\n"
         "#pragma once\n\n"
         "namespace dogip_gen {\n\n"
-        "template <int D, int P, int FORM> struct RefElem;\n\n");
+        "template <int D, int P, int FORM, int STORE> struct RefElem;\n\n");
     for (int d = 2; d <= 3; ++d)
-        for (int p = 1; p <= 4; ++p)
-            for (int form = 0; form <= 1; ++form) {
-                Table t = bhat_table(d, p, form);
-                const int VT = t.cols, WT = t.rows, NC = form == 0 ? 1 : d * (d + 1) / 2;
-                int nnz = 0, pm1 = 0;
-                for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
-                auto simp = cell_simplices(d);
-                auto A = multi_indices(d, p);
-                std::fprintf(f, "template <> struct RefElem<%d, %d, %d> {\n", d, p, form);
-                std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = %d, NS = %d;\n", VT, WT, NC, (int)simp.size());
-                std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
-                // lattice offsets
-                std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
-                for (size_t s = 0; s < simp.size(); ++s) {
-                    std::fprintf(f, "%s{", s ? ", " : "");
-                    for (int l = 0; l < VT; ++l) {
-                        std::fprintf(f, "%s{", l ? "," : "");
-                        for (int ax = 0; ax < d; ++ax) {
-                            int o = 0;
-                            for (int i = 0; i <= d; ++i) o += A[l][i] * simp[s][i][ax];
-                            std::fprintf(f, "%s%d", ax ? "," : "", o);
-                        }
-                        std::fprintf(f, "}");
-                    }
-                    std::fprintf(f, "}");
-                }
-                std::fprintf(f, "};\n");
-                // body
-                std::fprintf(f,
-                    "    template <class Pol>\n"
-                    "    static __device__ __forceinline__ void body(const double* __restrict__ u,\n"
-                    "                                                double* __restrict__ y, Pol& pol) {\n");
-                int flops = 0;
-                for (int j = 0; j < WT; ++j) {
-                    std::fprintf(f, "        { pol.template begin<%d>();\n", j);
-                    // interpolation rows
-                    for (int b = 0; b < t.nblk; ++b) {
-                        std::vector<std::pair<int, Rat>> terms;
-                        for (int l = 0; l < VT; ++l)
-                            if (!t.at(b, j, l).is_zero()) terms.push_back({l, t.at(b, j, l)});
-                        flops += emit_combo(f, "          ", "g" + std::to_string(b), true, terms, "u");
-                    }
-                    // weight multiply
-                    if (form == 0) {
-                        std::fprintf(f, "          const double h0 = pol.w(%d) * g0;\n", j);
-                        flops += 1;
-                    } else {
-                        // symmetric block rows k = j*NC + c, c over the upper triangle
-                        int idx[3][3], c = 0;
-                        for (int r = 0; r < d; ++r)
-                            for (int s = r; s < d; ++s) { idx[r][s] = idx[s][r] = c++; }
-                        for (int k = 0; k < NC; ++k)
-                            std::fprintf(f, "          const double a%d = pol.w(%d);\n", k, j * NC + k);
-                        for (int r = 0; r < d; ++r) {
-                            std::fprintf(f, "          const double h%d = ", r);
-                            std::string acc = "a" + std::to_string(idx[r][0]) + " * g0";
-                            for (int s = 1; s < d; ++s)
-                                acc = "__fma_rn(a" + std::to_string(idx[r][s]) + ", g" + std::to_string(s) + ", " + acc + ")";
-                            std::fprintf(f, "%s;\n", acc.c_str());
-                            flops += 2 * d - 1;
-                        }
-                    }
-                    // projection y_l += sum_b Bhat[b][j][l] h_b
-                    for (int l = 0; l < VT; ++l) {
-                        std::string acc = "y[" + std::to_string(l) + "]";
-                        bool any = false;
-                        for (int b = 0; b < t.nblk; ++b) {
-                            Rat c = t.at(b, j, l);
-                            if (c.is_zero()) continue;
-                            any = true;
-                            std::string h = "h" + std::to_string(b);
-                            if (c == Rat(1)) acc = "(" + acc + ") + " + h;
-                            else if (c == Rat(-1)) acc = "(" + acc + ") - " + h;
-                            else { acc = "__fma_rn(" + lit(c.to_double()) + ", " + h + ", " + acc + ")"; flops += 1; }
-                            flops += 1;
-                        }
-                        if (any) std::fprintf(f, "          y[%d] = %s;\n", l, acc.c_str());
-                    }
-                    std::fprintf(f, "          pol.template end<%d>(); }\n", j);
-                }
-                std::fprintf(f, "    }\n");
-                std::fprintf(f, "    static constexpr int FLOPS = %d;\n", flops);
-                std::fprintf(f, "};\n\n");
-            }
+        for (int p = 1; p <= 4; ++p) {
+            emit_variant(f, d, p, 0, 0);
+            emit_variant(f, d, p, 1, 0);
+            emit_variant(f, d, p, 1, 1);
+        }
     std::fprintf(f, "}  // namespace dogip_gen\n");
     std::fclose(f);
     return 0;

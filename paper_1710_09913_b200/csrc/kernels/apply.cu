@@ -21,7 +21,16 @@
 //    scatter (the boundary rows are fixed by dirichlet_fixup).
 #include <cuda_runtime.h>
 
+#ifdef DOGIP_GEN_HEADER
+#include DOGIP_GEN_HEADER
+#else
 #include "../generated/bhat_gen.cuh"
+#endif
+#ifndef DOGIP_UPREFETCH
+// cp.async (LDGSTS) prefetch of the next tile's u_T into shared memory.  Measured
+// slower than direct read-only gathers on B200 (profiles/r01_ab_variants.log), off.
+#define DOGIP_UPREFETCH 0
+#endif
 #include "apply.cuh"
 #include "common.cuh"
 
@@ -31,12 +40,10 @@ namespace {
 
 template <class RE>
 struct Chunking {
-    static constexpr int NC = RE::NC;
-    static constexpr int CHN = (12 / NC) < 1 ? 1 : (12 / NC);    // nodes per chunk
-    static constexpr int ROWS = CHN * NC;                        // rows per full chunk
-    static constexpr int NCH = (RE::WT + CHN - 1) / CHN;         // chunks per tile
-    static constexpr int TILE_ROWS = RE::WT * NC;
-    static constexpr int S = 4;                                  // ring stages per warp
+    static constexpr int ROWS = RE::ROWS;                                 // rows per streamed chunk
+    static constexpr int TILE_ROWS = RE::TILE_ROWS;                       // rows per tile
+    static constexpr int NCH = (TILE_ROWS + ROWS - 1) / ROWS;             // chunks per tile
+    static constexpr int S = 4;                                           // ring stages per warp
 };
 
 template <class RE>
@@ -65,9 +72,10 @@ struct WarpStream {
                              wbase + ((size_t)tile * C::TILE_ROWS + (size_t)c * C::ROWS) * TILE,
                              bytes, bar, policy);
     }
+    // node J's weights start a new chunk (node 0 also covers the NG leading rows)
     template <int J>
     __device__ __forceinline__ void begin() {
-        if constexpr (J % C::CHN == 0) {
+        if constexpr (J == 0 || RE::row_of(J) / C::ROWS != RE::row_of(J - 1) / C::ROWS) {
             __syncwarp();
             if (lane == 0) {
                 fence_proxy_async_smem();          // prior generic reads of the stage
@@ -84,16 +92,21 @@ struct WarpStream {
     __device__ __forceinline__ double w(int k) const { return cur[(k % C::ROWS) * TILE]; }
 };
 
-template <int D, int P, int F, bool DIR>
-__global__ void __launch_bounds__(APPLY_THREADS)
+// 3 CTAs (12 warps) per SM where u_T + y_T fit in <= 170 registers, else 2
+template <int D, int P, int F, int ST>
+constexpr int min_blocks() { return dogip_gen::RefElem<D, P, F, ST>::VT <= 20 ? 3 : 2; }
+
+template <int D, int P, int F, int ST, bool DIR>
+__global__ void __launch_bounds__(APPLY_THREADS, min_blocks<D, P, F, ST>())
 apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
              const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end) {
-    using RE = dogip_gen::RefElem<D, P, F>;
+    using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* rings = reinterpret_cast<double*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * C::S * C::ROWS * TILE * 8);
+    double* ubufs = rings + (size_t)NW * C::S * C::ROWS * TILE;          // [NW][VT][32]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ubufs + (size_t)NW * RE::VT * TILE);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpStream<RE> ws;
@@ -106,11 +119,26 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     ws.tile_end = tile_end;
     ws.g_cons = 0;
     ws.policy = policy_evict_first();
+    double* ubuf = ubufs + (size_t)warp * RE::VT * TILE;
+    const uint32_t ubuf_s = smem_u32(ubuf + lane);
     if (lane == 0) {
         for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
         fence_mbar_init();
-        for (int s = 0; s < C::S - 1; ++s) ws.issue(s);      // prologue
+        for (int s = 0; s < C::S - 1; ++s) ws.issue(s);      // prologue of the weight stream
     }
+    // u_T of a tile -> this lane's column of the warp's u buffer (cp.async, no registers)
+    auto prefetch_u = [&](int64_t t) {
+        const TileCoord tc = tile_coord(geo, t);
+        const int ci = tc.ci0 + lane;
+        if (ci < geo.Nx) {
+            const double* ub = u + (int64_t)geo.p * (ci + geo.sy * tc.cj + geo.sz * tc.ck);
+            const int* off = tab.off + tc.s * MAX_VT;
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) cp_async8(ubuf_s + 8u * TILE * l, ub + off[l]);
+        }
+        cp_async_commit();
+    };
+    if (DOGIP_UPREFETCH && ws.gw < tile_end) prefetch_u(ws.gw);
     __syncwarp();
 
     for (int64_t tile = ws.gw; tile < tile_end; tile += ws.nw) {
@@ -122,6 +150,10 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
         const int* lof = tab.loff + tc.s * MAX_VT;
         double uT[RE::VT], yT[RE::VT];
         uint64_t bmask = 0;
+        if (DOGIP_UPREFETCH) {
+            cp_async_wait_all();
+            __syncwarp();
+        }
 #pragma unroll
         for (int l = 0; l < RE::VT; ++l) {
             bool take = valid;
@@ -138,8 +170,17 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
                 }
                 if (b) { bmask |= (1ull << l); take = false; }
             }
-            uT[l] = take ? ldg_f64(u + base + off[l]) : 0.0;
+            if (DOGIP_UPREFETCH) {
+                const double v = ubuf[l * TILE + lane];
+                uT[l] = take ? v : 0.0;
+            } else {
+                uT[l] = take ? ldg_f64(u + base + off[l]) : 0.0;
+            }
             yT[l] = 0.0;
+        }
+        if (DOGIP_UPREFETCH) {
+            __syncwarp();
+            if (tile + ws.nw < tile_end) prefetch_u(tile + ws.nw);  // overlaps this tile's compute
         }
         RE::body(uT, yT, ws);
         if (valid) {
@@ -152,13 +193,14 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     }
 }
 
-template <int D, int P, int F, bool DIR>
+template <int D, int P, int F, int ST, bool DIR>
 cudaError_t launch_one(const ApplyArgs& a) {
-    using RE = dogip_gen::RefElem<D, P, F>;
+    using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
-    const size_t smem = (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8;
-    auto kern = apply_kernel<D, P, F, DIR>;
+    const size_t smem = (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * RE::VT * TILE * 8 +
+                        (size_t)NW * C::S * 8;
+    auto kern = apply_kernel<D, P, F, ST, DIR>;
     static int configured = 0;   // per instantiation
     static int occ = 1;
     if (!configured) {
@@ -180,14 +222,15 @@ cudaError_t launch_one(const ApplyArgs& a) {
     return cudaGetLastError();
 }
 
-template <int D, int P, int F>
+template <int D, int P, int F, int ST>
 cudaError_t launch_dir(const ApplyArgs& a) {
-    return a.dirichlet ? launch_one<D, P, F, true>(a) : launch_one<D, P, F, false>(a);
+    return a.dirichlet ? launch_one<D, P, F, ST, true>(a) : launch_one<D, P, F, ST, false>(a);
 }
 
 template <int D, int P>
 cudaError_t launch_form(const ApplyArgs& a) {
-    return a.form == 0 ? launch_dir<D, P, 0>(a) : launch_dir<D, P, 1>(a);
+    if (a.form == 0) return launch_dir<D, P, 0, 0>(a);
+    return a.store == 1 ? launch_dir<D, P, 1, 1>(a) : launch_dir<D, P, 1, 0>(a);
 }
 
 template <int D>
@@ -210,22 +253,27 @@ cudaError_t launch_apply(const ApplyArgs& a) {
 }
 
 // Reference-element constants of the generated tables, for the host side.
-template <int D, int P, int F>
+template <int D, int P, int F, int ST>
 static void fill_info(RefInfo& r) {
-    using RE = dogip_gen::RefElem<D, P, F>;
-    r.VT = RE::VT; r.WT = RE::WT; r.NC = RE::NC; r.NS = RE::NS;
+    using RE = dogip_gen::RefElem<D, P, F, ST>;
+    r.VT = RE::VT; r.WT = RE::WT; r.NC = RE::NC; r.NG = RE::NG; r.NS = RE::NS;
+    r.tile_rows = RE::TILE_ROWS;
     r.flops = RE::FLOPS; r.nnz = RE::NNZ; r.nnz_pm1 = RE::NNZ_PM1;
     for (int s = 0; s < RE::NS; ++s)
         for (int l = 0; l < RE::VT; ++l)
             for (int ax = 0; ax < 3; ++ax) r.loff[s][l][ax] = ax < D ? RE::LOFF[s][l][ax] : 0;
 }
 
-bool ref_info(int d, int p, int form, RefInfo& r) {
-#define DOGIP_CASE(D, P, F) if (d == D && p == P && form == F) { fill_info<D, P, F>(r); return true; }
-    DOGIP_CASE(2, 1, 0) DOGIP_CASE(2, 1, 1) DOGIP_CASE(2, 2, 0) DOGIP_CASE(2, 2, 1)
-    DOGIP_CASE(2, 3, 0) DOGIP_CASE(2, 3, 1) DOGIP_CASE(2, 4, 0) DOGIP_CASE(2, 4, 1)
-    DOGIP_CASE(3, 1, 0) DOGIP_CASE(3, 1, 1) DOGIP_CASE(3, 2, 0) DOGIP_CASE(3, 2, 1)
-    DOGIP_CASE(3, 3, 0) DOGIP_CASE(3, 3, 1) DOGIP_CASE(3, 4, 0) DOGIP_CASE(3, 4, 1)
+bool ref_info(int d, int p, int form, int store, RefInfo& r) {
+#define DOGIP_CASE(D, P)                                                       \
+    if (d == D && p == P) {                                                    \
+        if (form == 0 && store == 0) { fill_info<D, P, 0, 0>(r); return true; } \
+        if (form == 1 && store == 0) { fill_info<D, P, 1, 0>(r); return true; } \
+        if (form == 1 && store == 1) { fill_info<D, P, 1, 1>(r); return true; } \
+        return false;                                                          \
+    }
+    DOGIP_CASE(2, 1) DOGIP_CASE(2, 2) DOGIP_CASE(2, 3) DOGIP_CASE(2, 4)
+    DOGIP_CASE(3, 1) DOGIP_CASE(3, 2) DOGIP_CASE(3, 3) DOGIP_CASE(3, 4)
 #undef DOGIP_CASE
     return false;
 }

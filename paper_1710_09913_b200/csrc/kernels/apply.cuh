@@ -24,7 +24,7 @@ struct ApplyTables {
 };
 
 struct ApplyArgs {
-    int d, p, form;
+    int d, p, form, store;      // store: 0 full A_T blocks, 1 isotropic a_j + G_T (EL)
     bool dirichlet;
     const double* u;
     double* y;
@@ -40,14 +40,15 @@ cudaError_t launch_apply(const ApplyArgs& a);
 
 // Constants of the generated reference element (generated/bhat_gen.cuh).
 struct RefInfo {
-    int VT, WT, NC, NS, flops, nnz, nnz_pm1;
+    int VT, WT, NC, NG, NS, tile_rows, flops, nnz, nnz_pm1;
     int loff[MAX_NS][MAX_VT][3];
 };
-bool ref_info(int d, int p, int form, RefInfo& r);
+bool ref_info(int d, int p, int form, int store, RefInfo& r);
 
 // ----------------------------------------------------------- weights (K1)
 struct WeightsArgs {
-    int d, p, form, nq, WT, NC, ncomp;     // ncomp: coefficient components (1 or d(d+1)/2)
+    int d, p, form, store, nq, WT, NC, ncomp;  // ncomp: coefficient components (1 or d(d+1)/2)
+    int NG, tile_rows;                     // leading per-element rows, rows per tile
     int kind;                              // DOGIP_COEF_*
     const double* params;                  // device copy of the coefficient parameters
     int nparams;

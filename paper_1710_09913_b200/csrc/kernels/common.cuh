@@ -94,6 +94,13 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
 
+// Ampere-style async copy global -> shared (LDGSTS), 8 bytes, L1-allocating
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void red_add_f64(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }

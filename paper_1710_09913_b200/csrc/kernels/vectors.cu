@@ -25,12 +25,33 @@ __device__ __forceinline__ double block_sum(double v) {
     return v;
 }
 
+// Streaming kernels work on double2 pairs (vectors are 16-byte aligned:
+// cudaMalloc / torch allocations), U pairs in flight per thread; element i is
+// in pair i/2.  The [i0, i1) owned-range mask applies per element.
+constexpr int VU = 2;
+
 __global__ void __launch_bounds__(RED_THREADS) dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                                           int64_t i0, int64_t i1, double* partials) {
+    const double2* a2 = reinterpret_cast<const double2*>(a);
+    const double2* b2 = reinterpret_cast<const double2*>(b);
+    const int64_t k0 = i0 / 2, k1 = (i1 + 1) / 2;
+    const int64_t stride = (int64_t)gridDim.x * RED_THREADS;
     double s = 0.0;
-    for (int64_t i = i0 + (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < i1;
-         i += (int64_t)gridDim.x * RED_THREADS)
-        s = fma(a[i], b[i], s);
+    for (int64_t k = k0 + (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < k1; k += VU * stride) {
+        double2 va[VU], vb[VU];
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk < k1) { va[j] = a2[kk]; vb[j] = b2[kk]; }
+            else { va[j] = make_double2(0.0, 0.0); vb[j] = va[j]; }
+        }
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t e = 2 * (k + j * stride);
+            if (e >= i0 && e < i1) s = fma(va[j].x, vb[j].x, s);
+            if (e + 1 >= i0 && e + 1 < i1) s = fma(va[j].y, vb[j].y, s);
+        }
+    }
     s = block_sum(s);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
@@ -47,12 +68,42 @@ __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__
                                                             const double* __restrict__ q, int64_t n, int64_t i0,
                                                             int64_t i1, const double* scal, double* partials) {
     const double alpha = scal[S_RR] / scal[S_PQ];
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* q2 = reinterpret_cast<const double2*>(q);
+    const int64_t np = n / 2;
+    const int64_t stride = (int64_t)gridDim.x * RED_THREADS;
+    const int64_t tid = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x;
     double s = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * RED_THREADS) {
-        x[i] = fma(alpha, p[i], x[i]);
-        const double ri = fma(-alpha, q[i], r[i]);
-        r[i] = ri;
-        if (i >= i0 && i < i1) s = fma(ri, ri, s);
+    for (int64_t k = tid; k < np; k += VU * stride) {
+        double2 vx[VU], vr[VU], vp[VU], vq[VU];
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk < np) { vx[j] = x2[kk]; vr[j] = r2[kk]; vp[j] = p2[kk]; vq[j] = q2[kk]; }
+        }
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk >= np) continue;
+            vx[j].x = fma(alpha, vp[j].x, vx[j].x);
+            vx[j].y = fma(alpha, vp[j].y, vx[j].y);
+            vr[j].x = fma(-alpha, vq[j].x, vr[j].x);
+            vr[j].y = fma(-alpha, vq[j].y, vr[j].y);
+            x2[kk] = vx[j];
+            r2[kk] = vr[j];
+            const int64_t e = 2 * kk;
+            if (e >= i0 && e < i1) s = fma(vr[j].x, vr[j].x, s);
+            if (e + 1 >= i0 && e + 1 < i1) s = fma(vr[j].y, vr[j].y, s);
+        }
+    }
+    if ((n & 1) && tid == 0) {          // odd tail element
+        const int64_t e = n - 1;
+        x[e] = fma(alpha, p[e], x[e]);
+        const double re = fma(-alpha, q[e], r[e]);
+        r[e] = re;
+        if (e >= i0 && e < i1) s = fma(re, re, s);
     }
     s = block_sum(s);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
@@ -61,8 +112,28 @@ __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__
 __global__ void __launch_bounds__(RED_THREADS) cg_p_kernel(double* __restrict__ p, const double* __restrict__ r,
                                                            int64_t n, const double* scal) {
     const double beta = scal[S_RRNEW] / scal[S_RR];
-    for (int64_t i = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; i < n; i += (int64_t)gridDim.x * RED_THREADS)
-        p[i] = fma(beta, p[i], r[i]);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const int64_t np = n / 2;
+    const int64_t stride = (int64_t)gridDim.x * RED_THREADS;
+    const int64_t tid = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x;
+    for (int64_t k = tid; k < np; k += VU * stride) {
+        double2 vp[VU], vr[VU];
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk < np) { vp[j] = p2[kk]; vr[j] = r2[kk]; }
+        }
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk >= np) continue;
+            vp[j].x = fma(beta, vp[j].x, vr[j].x);
+            vp[j].y = fma(beta, vp[j].y, vr[j].y);
+            p2[kk] = vp[j];
+        }
+    }
+    if ((n & 1) && tid == 0) p[n - 1] = fma(beta, p[n - 1], r[n - 1]);
 }
 
 __global__ void shift_rr_kernel(double* scal) { scal[S_RR] = scal[S_RRNEW]; }

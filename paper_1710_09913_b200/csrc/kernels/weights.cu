@@ -239,7 +239,7 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
     const int d = a.d, WT = a.WT, NC = a.NC, nc = a.ncomp;
     const int64_t tile = eK / TILE;
     const int lane = (int)(eK % TILE);
-    double* out = a.out + (size_t)tile * WT * NC * TILE + lane;
+    double* out = a.out + (size_t)tile * a.tile_rows * TILE + lane;
     double cconst[6] = {0, 0, 0, 0, 0, 0};
     if (direct) {
         double x[3] = {G.S[0], G.S[1], G.S[2]};
@@ -247,6 +247,22 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
         if (G.valid && !coef_ok(nc, d, cconst)) atomicOr(a.bad_flag, 2);
     }
     const double adet = fabs(G.det);
+    if (a.store == 1) {
+        // isotropic storage (Corollary P:411-428, element-wise): G_T = Rinv Rinv^T, then a_j
+        int o = 0;
+        for (int r = 0; r < d; ++r)
+            for (int s = r; s < d; ++s) {
+                double v = 0.0;
+                for (int q = 0; q < d; ++q) v += G.Rinv[r][q] * G.Rinv[s][q];
+                out[(size_t)o * TILE] = G.valid ? v : 0.0;
+                ++o;
+            }
+        for (int j = 0; j < WT; ++j) {
+            const double aj = direct ? adet * cconst[0] * a.sW[j] : a.scratch_a[el * WT + j];
+            out[(size_t)(a.NG + j) * TILE] = G.valid ? aj : 0.0;
+        }
+        return;
+    }
     for (int j = 0; j < WT; ++j) {
         double ab[6];
         for (int c = 0; c < nc; ++c)

@@ -1,0 +1,106 @@
+#!/usr/bin/env python
+"""Per-config measurements on one GPU (DESIGN.md tables): apply time, algorithmic
+GB/s and fraction of the measured HBM copy bandwidth, CG s/iter, and the full CG
+solves BASELINE.json asks for (C1 EL Dirichlet 1e-10, C3 EL Dirichlet 1e-10,
+C5 WP mass 1e-12), each followed by a GPU-side true-residual check.
+
+    python scripts/config_sweep.py [--configs C1,C2p1,...] [--solve] [--iters 20]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1710_09913_b200.api import Mesh, Operator  # noqa: E402
+from synth.configs import get_config  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def time_apply(op, u, y, n, dirichlet):
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        op.apply(u, y, dirichlet=dirichlet)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(n):
+        op.apply(u, y, dirichlet=dirichlet)
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / n
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C1,C2p1,C2p2,C2p3,C2p4,C3,C4,C5")
+    ap.add_argument("--solve", action="store_true")
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--iso", action="store_true", help="also the isotropic compressed EL storage")
+    args = ap.parse_args()
+    rows = []
+    for name in args.configs.split(","):
+        c = get_config(name)
+        forms = c.forms
+        t0 = time.time()
+        coef = c.coefficient()
+        mesh = Mesh(c.d, c.N, c.p, c.vertices())
+        variants = [(f, 0) for f in forms]
+        if args.iso and coef.isotropic and 1 in forms:
+            variants.append((1, 1))
+        for form, storage in variants:
+            op = Operator(mesh, form, coef, storage=storage)
+            oi = op.info
+            u = torch.from_numpy(c.u()).cuda()
+            y = torch.empty_like(u)
+            dirichlet = form == 1
+            n = args.iters if c.ndof > 1e6 else 200
+            t_apply = time_apply(op, u, y, n, dirichlet)
+            nw = oi["W_T"] * oi["n_c"] if storage == 0 else oi["W_T"] + oi["n_c"]
+            alg = 8 * nw * c.n_elem + 16 * c.ndof
+            b = op.load_vector(1.0, dirichlet=dirichlet)
+            x = torch.zeros_like(b)
+            op.cg(b, x, maxit=-3, dirichlet=dirichlet)
+            r = op.cg(b, x, maxit=-n, dirichlet=dirichlet, resume=True)
+            row = {"config": name, "form": "WP" if form == 0 else ("EL" if storage == 0 else "EL-iso"),
+                   "d": c.d, "N": c.N, "p": c.p, "flops_per_elem": oi["flops_per_elem"],
+                   "fp64_TFs": oi["flops_per_elem"] * c.n_elem / t_apply / 1e12,
+                   "n_elem": c.n_elem, "ndof": c.ndof, "W_T": oi["W_T"], "n_c": oi["n_c"],
+                   "weights_GB": oi["weight_bytes"] / 1e9, "weights_ms": oi["weights_ms"],
+                   "apply_ms": t_apply * 1e3, "GDoF_s": c.ndof / t_apply / 1e9,
+                   "alg_GB": alg / 1e9, "alg_GBs": alg / t_apply / 1e9, "frac_measured": alg / t_apply / 1e9 / PEAK,
+                   "cg_ms_per_iter": r["seconds"] / n * 1e3, "cg_apply_ms": r["apply_seconds"] / n * 1e3}
+            if args.solve and (name in ("C1", "C3", "C5")) and (name != "C1" or form == 1):
+                tol = 1e-12 if name == "C5" else 1e-10
+                x = torch.zeros_like(b)
+                res = op.cg(b, x, rtol=tol, maxit=200000, dirichlet=dirichlet)
+                yx = op.apply(x, dirichlet=dirichlet)
+                true_res = (torch.linalg.vector_norm(b - yx) / torch.linalg.vector_norm(b)).item()
+                row.update({"solve_tol": tol, "solve_iters": res["iters"], "solve_status": res["status"],
+                            "solve_rel_res": res["rel_res"], "solve_true_rel_res": true_res,
+                            "solve_s": res["seconds"]})
+            row["wall_s"] = time.time() - t0
+            print(json.dumps(row), flush=True)
+            rows.append(row)
+            op.close()
+            del u, y, b, x
+            torch.cuda.empty_cache()
+        mesh.close()
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(rows, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -277,3 +277,56 @@ def test_error_codes_on_gpu():
     with pytest.raises(DogipError) as ei:
         Operator(m2, 1, CoeffSpec(COEF_CONST, np.array([1.0])))
     assert ei.value.code == -4
+
+
+ISO_CASES = [(2, 20, 2, "sincos"), (2, 9, 4, "grf"), (3, 3, 3, "tanh"), (3, 2, 4, "grf"), (3, 4, 1, "tanh")]
+
+
+@pytest.mark.parametrize("d,N,p,kind", ISO_CASES)
+def test_iso_storage_matches_oracle(d, N, p, kind):
+    """DOGIP_STORE_ISO (Corollary P:411-428, element-wise: A_{T,j} = a_{T,j} G_T):
+    same operator as the assembled A, expanded weights equal the oracle's."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    coef = {"sincos": SINCOS, "tanh": TANH2 if d == 2 else TANH3,
+            "grf": Coefficient(COEF_PER_CELL, np.zeros(0), grf_per_cell(d, N, 0.05, 1.0, 1))}[kind]
+    verts = jitter_verts(d, N)
+    m = Mesh(d, N, p, verts)
+    op = Operator(m, 1, coef, storage=1)
+    assert op.info["storage"] == 1 and op.info["stream_doubles_per_elem"] == op.info["W_T"] + d * (d + 1) // 2
+    ed = oa.build(d, N, p, verts)
+    A = oa.assemble_csr(ed, 1, coef)
+    u = u_vector(ed.ndof, 0)
+    y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    assert relerr(y, A @ u) <= TOL
+    ref = od.element_weights(ed, 1, coef)
+    iu = np.triu_indices(d)
+    assert relerr(op.export_weights(), ref[:, :, iu[0], iu[1]]) <= 1e-13
+    mask = boundary_mask(d, N, p)
+    yd = op.apply(torch.from_numpy(u).cuda(), dirichlet=True).cpu().numpy()
+    assert relerr(yd, oa.dirichlet_matrix(A, mask) @ u) <= TOL
+
+
+def test_iso_storage_full_size_c4_sampled():
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config("C4")
+    coef = c.coefficient()
+    m = Mesh(3, c.N, c.p)
+    op = Operator(m, 1, coef, storage=1)
+    u = c.u()
+    y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    rows = np.unique(np.random.default_rng(12).integers(0, c.ndof, 40))
+    ref = oa.apply_rows_sampled(3, c.N, c.p, None, 1, coef, u, rows)
+    assert np.abs(y[rows] - ref).max() / np.abs(y).max() <= TOL
+
+
+def test_iso_storage_errors():
+    from paper_1710_09913_b200.api import DogipError, Mesh, Operator
+    m = Mesh(3, 2, 2)
+    with pytest.raises(DogipError) as ei:
+        Operator(m, 1, ANISO, storage=1)
+    assert ei.value.code == -5
+    with pytest.raises(DogipError) as ei:
+        Operator(m, 0, TANH3, storage=1)
+    assert ei.value.code == -10
