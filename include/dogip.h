@@ -245,6 +245,13 @@ int dogip_reference_table(int d, int p, int form, double* out, int64_t cap);
 /* nnz and nnz_{+-1} of the reference table (eq:comp_eff; reading L12). */
 int dogip_reference_nnz(int d, int p, int form, int64_t* nnz, int64_t* nnz_pm1);
 
+/* Structural nonzeros of the assembled CSR matrix A of C_{N,p} on M_N (pairs of
+ * DoFs sharing an element, the full pattern), exact: counted for small N and
+ * extended through the exact degree-d polynomial in N it follows.  With the
+ * paper's memory model mem A = 2 nnz + nrows this reproduces the `mem A`
+ * column of Tables 3/4.  p <= 8 (2D), <= 6 (3D).  Host only. */
+int dogip_csr_nnz(int d, int64_t N, int p, int64_t* nnz);
+
 /* The collapsed Gauss-Jacobi rule: pts (n1d^d x d), wts (n1d^d).  Returns n1d^d. */
 int dogip_quadrature(int d, int n1d, double* pts, double* wts, int64_t cap);
 

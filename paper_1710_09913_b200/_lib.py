@@ -68,6 +68,7 @@ SIGNATURES = [
     ("dogip_kernel_launches", C.c_int64, []),
     ("dogip_reference_table", C.c_int, [C.c_int, C.c_int, C.c_int, c_dp, C.c_int64]),
     ("dogip_reference_nnz", C.c_int, [C.c_int, C.c_int, C.c_int, c_i64p, c_i64p]),
+    ("dogip_csr_nnz", C.c_int, [C.c_int, C.c_int64, C.c_int, c_i64p]),
     ("dogip_quadrature", C.c_int, [C.c_int, C.c_int, c_dp, c_dp, C.c_int64]),
     ("dogip_export_weights", C.c_int, [C.c_void_p, c_dp, C.c_int64]),
     ("dogip_export_dofmap", C.c_int, [C.c_void_p, c_i64p, C.c_int64]),

@@ -73,6 +73,8 @@ struct dogip_op_s {
     double* h_scal = nullptr;  // pinned
     double* hu = nullptr;      // device scratch for the host-buffer apply
     double* hy = nullptr;
+    double* dotp = nullptr;    // per-warp partials of p^T A p (3 launches x APPLY_MAX_WARPS)
+    double* bpart = nullptr;   // boundary-row partials of the Dirichlet fix-up (RED_BLOCKS)
     float weights_ms = 0.f;
 };
 
@@ -381,7 +383,9 @@ extern "C" int dogip_op_info(dogip_op op, dogip_op_info_t* o) {
 extern "C" void dogip_op_destroy(dogip_op op) {
     if (!op) return;
     cudaSetDevice(op->m->device);
-    for (double* x : {op->d_w, op->d_sV, op->r, op->pv, op->q, op->partials, op->scal, op->hu, op->hy}) cudaFree(x);
+    for (double* x : {op->d_w, op->d_sV, op->r, op->pv, op->q, op->partials, op->scal, op->hu, op->hy, op->dotp,
+                      op->bpart})
+        cudaFree(x);
     if (op->h_scal) cudaFreeHost(op->h_scal);
     delete op;
 }
@@ -415,7 +419,10 @@ static int finish_exchange(dogip_mesh_s* m, double* y, cudaStream_t st) {
     return DOGIP_OK;
 }
 
-static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, cudaStream_t st) {
+// y = A u (+ exchange); with dot != null also *dot = u^T y over this rank's elements
+// (+ boundary rows owned by this rank), fused into the apply kernel (CG's p.q).
+static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, cudaStream_t st,
+                      double* dot = nullptr) {
     dogip_mesh_s* m = op->m;
     const SlabGeo& g = m->geo;
     CK(cudaMemsetAsync(y, 0, sizeof(double) * g.ndof, st));
@@ -425,32 +432,54 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
     a.u = u; a.y = y; a.w = op->d_w; a.geo = g; a.tab = &m->tab;
     a.num_sms = m->num_sms;
     a.stream = st;
+    int nslots[3] = {0, 0, 0};
+    int nl = 0;
+    if (dot && !op->dotp) {
+        CK(cudaMalloc(&op->dotp, sizeof(double) * 3 * APPLY_MAX_WARPS));
+        CK(cudaMalloc(&op->bpart, sizeof(double) * RED_BLOCKS));
+    }
+    auto launch = [&](int64_t t0, int64_t t1) -> cudaError_t {
+        a.tile_begin = t0;
+        a.tile_end = t1;
+        a.dot_partials = dot ? op->dotp + (size_t)nl * APPLY_MAX_WARPS : nullptr;
+        a.dot_nslots = &nslots[nl];
+        ++nl;
+        return launch_apply(a);
+    };
     const bool xchg = m->nranks > 1 && m->comm && !(flags & DOGIP_NO_EXCHANGE);
     if (!xchg) {
-        a.tile_begin = 0; a.tile_end = g.ntiles;
-        CK(launch_apply(a));
+        CK(launch(0, g.ntiles));
     } else {
         // boundary cube layers first, exchange overlapped with the interior layers
         const int64_t layers = m->z1 - m->z0;
         const int64_t tpl = g.ntiles / layers;
         if (layers <= 2) {
-            a.tile_begin = 0; a.tile_end = g.ntiles;
-            CK(launch_apply(a));
+            CK(launch(0, g.ntiles));
             CK(cudaEventRecord(m->ev_bnd, st));
             RET(exchange_planes(m, y, m->ev_bnd));
         } else {
-            a.tile_begin = 0; a.tile_end = tpl;
-            CK(launch_apply(a));
-            a.tile_begin = g.ntiles - tpl; a.tile_end = g.ntiles;
-            CK(launch_apply(a));
+            CK(launch(0, tpl));
+            CK(launch(g.ntiles - tpl, g.ntiles));
             CK(cudaEventRecord(m->ev_bnd, st));
             RET(exchange_planes(m, y, m->ev_bnd));
-            a.tile_begin = tpl; a.tile_end = g.ntiles - tpl;
-            CK(launch_apply(a));
+            CK(launch(tpl, g.ntiles - tpl));
         }
         RET(finish_exchange(m, y, st));
     }
-    if (a.dirichlet) CK(launch_dirichlet_fixup(g, u, y, st));
+    if (dot) {
+        for (int i = 0; i < nl; ++i)
+            CK(launch_sum_partials(op->dotp + (size_t)i * APPLY_MAX_WARPS, nslots[i], i ? dot : nullptr, dot, st));
+    }
+    if (a.dirichlet) {
+        if (dot) {
+            dogip_mesh_info_t info;
+            dogip_mesh_info(m, &info);
+            CK(launch_dirichlet_fixup_dot(g, u, y, info.owned_begin, info.owned_end, op->bpart, st));
+            CK(launch_sum_partials(op->bpart, RED_BLOCKS, dot, dot, st));
+        } else {
+            CK(launch_dirichlet_fixup(g, u, y, st));
+        }
+    }
     return DOGIP_OK;
 }
 
@@ -564,17 +593,16 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
         if (!bench && std::sqrt(rr) <= rtol * bnorm) break;
         if (it >= nit) { status = bench ? DOGIP_OK : DOGIP_NOT_CONVERGED; break; }
         if (bench) CK(cudaEventRecord(aev[2 * it], st));
-        RET(apply_impl(op, op->pv, op->q, aflags, st));                        // q = A p
+        RET(apply_impl(op, op->pv, op->q, aflags, st, op->scal + S_PQ));      // q = A p, p.q fused
         if (bench) CK(cudaEventRecord(aev[2 * it + 1], st));
-        CK(launch_dot(op->pv, op->q, o0, o1, op->partials, op->scal + S_PQ, st));
         RET(allreduce_scalar(m, op->scal + S_PQ, st));
-        CK(launch_cg_xr(x, op->r, op->pv, op->q, n, o0, o1, op->scal, op->partials, st));
+        CK(launch_cg_r(op->r, op->q, n, o0, o1, op->scal, op->partials, st));  // r -= alpha q, r.r
         RET(allreduce_scalar(m, op->scal + S_RRNEW, st));
         if (!bench) {
             CK(cudaMemcpyAsync(op->h_scal + S_PQ, op->scal + S_PQ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
             CK(cudaEventRecord(ready, st));
         }
-        CK(launch_cg_p(op->pv, op->r, n, op->scal, st));
+        CK(launch_cg_px(x, op->pv, op->r, n, op->scal, st));                  // x += alpha p, p = r + beta p
         ++it;
         if (!bench) {
             CK(cudaEventSynchronize(ready));
@@ -631,6 +659,73 @@ extern "C" int dogip_reference_nnz(int d, int p, int form, int64_t* nnz, int64_t
     for (auto& v : t.v) { a += !v.is_zero(); b += v.is_pm1(); }
     if (nnz) *nnz = a;
     if (pm1) *pm1 = b;
+    return DOGIP_OK;
+}
+
+// exact count of distinct DoF pairs sharing an element, structured mesh of n cells
+static int64_t csr_nnz_direct(int d, int64_t n, int p) {
+    const auto A = multi_indices(d, p);
+    const auto simp = cell_simplices(d);
+    struct RI {
+        int VT;
+        std::vector<std::array<std::array<int, 3>, 128>> loff;   // [s][l][axis], V_T <= 84
+    } ri;
+    ri.VT = (int)A.size();
+    ri.loff.resize(simp.size());
+    for (size_t s = 0; s < simp.size(); ++s)
+        for (int l = 0; l < ri.VT; ++l)
+            for (int ax = 0; ax < 3; ++ax) {
+                int o = 0;
+                for (int i = 0; i <= d; ++i) o += A[l][i] * simp[s][i][ax];
+                ri.loff[s][l][ax] = ax < d ? o : 0;
+            }
+    const int64_t M = p * n + 1;
+    const int ns = d == 2 ? 2 : 6;
+    const int64_t ncell = d == 2 ? n * n : n * n * n;
+    std::vector<uint64_t> keys;
+    keys.reserve((size_t)ncell * ns * ri.VT * ri.VT);
+    const uint64_t nd = (uint64_t)(d == 2 ? M * M : M * M * M);
+    std::vector<int64_t> ids(ri.VT);
+    for (int64_t c = 0; c < ncell; ++c) {
+        const int64_t ci = c % n, cj = (c / n) % n, ck = d == 3 ? c / (n * n) : 0;
+        for (int s = 0; s < ns; ++s) {
+            for (int l = 0; l < ri.VT; ++l) {
+                const auto& o = ri.loff[s][l];
+                ids[l] = (p * ci + o[0]) + M * (p * cj + o[1]) + (d == 3 ? M * M * (p * ck + o[2]) : 0);
+            }
+            for (int i = 0; i < ri.VT; ++i)
+                for (int j = 0; j < ri.VT; ++j) keys.push_back((uint64_t)ids[i] * nd + (uint64_t)ids[j]);
+        }
+    }
+    std::sort(keys.begin(), keys.end());
+    return (int64_t)(std::unique(keys.begin(), keys.end()) - keys.begin());
+}
+
+extern "C" int dogip_csr_nnz(int d, int64_t N, int p, int64_t* nnz) {
+    if (d != 2 && d != 3) return fail(DOGIP_E_INVALID_DIM, "d must be 2 or 3");
+    if (p < 1 || p > 8 || (d == 3 && p > 6)) return fail(DOGIP_E_UNSUPPORTED_ORDER, "p must be in 1..8 (2D), 1..6 (3D)");
+    if (N < 1 || !nnz) return fail(DOGIP_E_INVALID_SIZE, "N must be >= 1");
+    if (N <= d + 3) { *nnz = csr_nnz_direct(d, N, p); return DOGIP_OK; }
+    // nnz(N) is an exact polynomial of degree d for N >= 2: Lagrange through N = 2..d+3,
+    // checked on the extra point d+3 from the first d+1 samples
+    const int npt = d + 2;
+    std::vector<int64_t> xs(npt), ys(npt);
+    for (int i = 0; i < npt; ++i) { xs[i] = 2 + i; ys[i] = csr_nnz_direct(d, xs[i], p); }
+    auto lagrange = [&](int64_t x, int m) {
+        Rat acc(0);
+        for (int i = 0; i < m; ++i) {
+            Rat t(ys[i]);
+            for (int j = 0; j < m; ++j)
+                if (j != i) t = t * Rat(x - xs[j], xs[i] - xs[j]);
+            acc = acc + t;
+        }
+        return acc;
+    };
+    if (lagrange(xs[npt - 1], npt - 1) != Rat(ys[npt - 1]))
+        return fail(DOGIP_E_INVALID_ARG, "pattern count is not polynomial in N");
+    const Rat v = lagrange(N, npt);
+    if (v.d != 1) return fail(DOGIP_E_INVALID_ARG, "non-integer pattern count");
+    *nnz = v.n;
     return DOGIP_OK;
 }
 

@@ -32,14 +32,9 @@ static std::string lit(double v) {
     return s;
 }
 
-// emit "dst = sum_l c_l src[l]" for a sparse row; returns flop count
-static int emit_combo(FILE* f, const char* indent, const std::string& dst, bool declare,
-                      const std::vector<std::pair<int, Rat>>& terms, const char* src) {
-    int flops = 0;
-    if (terms.empty()) {
-        std::fprintf(f, "%s%s%s = 0.0;\n", indent, declare ? "const double " : "", dst.c_str());
-        return 0;
-    }
+static int g_split = 0;   // rows with >= g_split terms use two interleaved partial sums (argv[3]; 0 = off)
+
+static std::string chain(const std::vector<std::pair<int, Rat>>& terms, const char* src, int& flops) {
     bool first = true;
     std::string acc;   // a chain of fma for determinism and contraction control
     for (auto& t : terms) {
@@ -57,6 +52,28 @@ static int emit_combo(FILE* f, const char* indent, const std::string& dst, bool 
             flops += 1;
         }
     }
+    return acc;
+}
+
+// emit "dst = sum_l c_l src[l]" for a sparse row; returns flop count
+static int emit_combo(FILE* f, const char* indent, const std::string& dst, bool declare,
+                      const std::vector<std::pair<int, Rat>>& terms, const char* src) {
+    int flops = 0;
+    if (terms.empty()) {
+        std::fprintf(f, "%s%s%s = 0.0;\n", indent, declare ? "const double " : "", dst.c_str());
+        return 0;
+    }
+    if (g_split > 0 && (int)terms.size() >= g_split) {
+        // two independent half-chains (even / odd terms) joined by one add: more ILP
+        std::vector<std::pair<int, Rat>> a, b;
+        for (size_t i = 0; i < terms.size(); ++i) (i % 2 ? b : a).push_back(terms[i]);
+        const std::string ea = chain(a, src, flops), eb = chain(b, src, flops);
+        flops += 1;
+        std::fprintf(f, "%s%s%s = (%s) + (%s);\n", indent, declare ? "const double " : "", dst.c_str(), ea.c_str(),
+                     eb.c_str());
+        return flops;
+    }
+    const std::string acc = chain(terms, src, flops);
     std::fprintf(f, "%s%s%s = %s;\n", indent, declare ? "const double " : "", dst.c_str(), acc.c_str());
     return flops;
 }
@@ -191,6 +208,7 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
 int main(int argc, char** argv) {
     if (argc < 2) { std::fprintf(stderr, "usage: gen_bhat out.cuh [group_values]\n"); return 2; }
     if (argc > 2) g_gmax_vals = std::atoi(argv[2]);
+    if (argc > 3) g_split = std::atoi(argv[3]);
     FILE* f = std::fopen(argv[1], "w");
     if (!f) { std::perror("open"); return 1; }
     std::fprintf(f,

@@ -93,13 +93,17 @@ struct WarpStream {
 };
 
 // 3 CTAs (12 warps) per SM where u_T + y_T fit in <= 170 registers, else 2
+#ifndef DOGIP_MINB_LARGE
+#define DOGIP_MINB_LARGE 2   // CTAs/SM asked of ptxas when V_T > 20 (3D P4)
+#endif
 template <int D, int P, int F, int ST>
-constexpr int min_blocks() { return dogip_gen::RefElem<D, P, F, ST>::VT <= 20 ? 3 : 2; }
+constexpr int min_blocks() { return dogip_gen::RefElem<D, P, F, ST>::VT <= 20 ? 3 : DOGIP_MINB_LARGE; }
 
 template <int D, int P, int F, int ST, bool DIR>
 __global__ void __launch_bounds__(APPLY_THREADS, min_blocks<D, P, F, ST>())
 apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
-             const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end) {
+             const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end,
+             double* __restrict__ dot_partials) {
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
@@ -141,6 +145,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     if (DOGIP_UPREFETCH && ws.gw < tile_end) prefetch_u(ws.gw);
     __syncwarp();
 
+    double udot = 0.0;
     for (int64_t tile = ws.gw; tile < tile_end; tile += ws.nw) {
         const TileCoord tc = tile_coord(geo, tile);
         const int ci = tc.ci0 + lane;
@@ -189,7 +194,14 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
                 if (DIR && ((bmask >> l) & 1ull)) continue;
                 red_add_f64(y + base + off[l], yT[l]);
             }
+            // u^T A u = sum_T u_T^T (Bhat^T A_T Bhat u_T): the CG dot p.q, element by element
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) udot = fma(uT[l], yT[l], udot);
         }
+    }
+    if (dot_partials) {     // deterministic: one partial per warp, fixed order reduction later
+        for (int o = 16; o > 0; o >>= 1) udot += __shfl_xor_sync(0xffffffffu, udot, o);
+        if (lane == 0) dot_partials[(int64_t)blockIdx.x * NW + warp] = udot;
     }
 }
 
@@ -212,12 +224,18 @@ cudaError_t launch_one(const ApplyArgs& a) {
         configured = 1;
     }
     const int64_t ntiles = a.tile_end - a.tile_begin;
-    if (ntiles <= 0) return cudaSuccess;
     int64_t grid = (int64_t)a.num_sms * occ;
     const int64_t need = (ntiles + NW - 1) / NW;
     if (grid > need) grid = need;
+    if (a.dot_partials) {       // every slot of the partial array must be written
+        if (grid < 1) grid = 1;
+        if (grid * NW > APPLY_MAX_WARPS) grid = APPLY_MAX_WARPS / NW;
+        *a.dot_nslots = (int)(grid * NW);
+    } else if (ntiles <= 0) {
+        return cudaSuccess;
+    }
     kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, a.tile_begin,
-                                                           a.tile_end);
+                                                           a.tile_end, a.dot_partials);
     count_launches(1);
     return cudaGetLastError();
 }

@@ -14,6 +14,7 @@ extern std::atomic<long long> g_launches;
 inline void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 constexpr int APPLY_THREADS = 128;   // 4 warps = 4 tiles in flight per CTA
+constexpr int APPLY_MAX_WARPS = 148 * 8 * 4;   // bound of the per-warp dot partials of one launch
 
 // Warp-uniform gather tables (kernel-parameter bank): off = local DoF index
 // offset of local DoF l of simplex s from the cell's base DoF; loff = the
@@ -34,6 +35,8 @@ struct ApplyArgs {
     int64_t tile_begin, tile_end;
     int num_sms;
     cudaStream_t stream;
+    double* dot_partials;      // != null: per-warp partials of u^T A u (APPLY_MAX_WARPS slots)
+    int* dot_nslots;           // out: number of partial slots written
 };
 
 cudaError_t launch_apply(const ApplyArgs& a);
@@ -89,6 +92,17 @@ cudaError_t launch_axpby(double* y, const double* x, double a, double b, int64_t
 cudaError_t launch_add_planes(double* y, const double* lo, const double* hi, int64_t plane,
                               int64_t last_plane_off, cudaStream_t st);
 cudaError_t launch_fill(double* y, double v, int64_t n, cudaStream_t st);
+// sum of n partials in fixed order (+ *extra if non-null) -> *out
+cudaError_t launch_sum_partials(const double* partials, int n, const double* extra, double* out, cudaStream_t st);
+// Dirichlet rows y_i = u_i on boundary DoFs; if bpart != null also the partial sum of
+// u_i^2 over boundary DoFs in [i0, i1), each counted once (RED_BLOCKS slots)
+cudaError_t launch_dirichlet_fixup_dot(const SlabGeo& g, const double* u, double* y, int64_t i0, int64_t i1,
+                                       double* bpart, cudaStream_t st);
+// r -= alpha q (alpha = scal[RR]/scal[PQ]) over [0,n); partial r.r over [i0,i1) -> scal[RRNEW]
+cudaError_t launch_cg_r(double* r, const double* q, int64_t n, int64_t i0, int64_t i1, double* scal,
+                        double* partials, cudaStream_t st);
+// x += alpha p; p = r + beta p (beta = scal[RRNEW]/scal[RR]); then scal[RR] = scal[RRNEW]
+cudaError_t launch_cg_px(double* x, double* p, const double* r, int64_t n, double* scal, cudaStream_t st);
 
 enum CgScal { S_RR = 0, S_PQ = 1, S_RRNEW = 2, S_BB = 3, S_COUNT = 8 };
 

@@ -156,14 +156,18 @@ __global__ void add_planes_kernel(double* y, const double* lo, const double* hi,
     }
 }
 
-// Boundary DoFs of the local slab, enumerated face by face (duplicates on
-// edges are harmless: every face writes the same value).
-__device__ __forceinline__ bool boundary_dof(const SlabGeo& g, int64_t t, int64_t& idx) {
+// Boundary DoFs of the local slab, enumerated face by face.  Edge / corner DoFs
+// appear on several faces; `first` marks the one enumeration that counts them
+// (faces in order x0, x1, y0, y1, z0, z1; later faces skip earlier faces' DoFs).
+__device__ __forceinline__ bool boundary_dof(const SlabGeo& g, int64_t t, int64_t& idx, bool& first) {
     const int64_t nx = g.pmax_x + 1, ny = g.pmax_y + 1, nz = g.pmax_z + 1;
+    first = true;
     if (g.d == 2) {
         // faces x = 0, x = pmax_x over y; y = 0 (bnd_lo), y = pmax_y (bnd_hi) over x
         if (t < 2 * ny) { const int64_t Y = t % ny; idx = (t / ny ? g.pmax_x : 0) + Y * g.sy; return true; }
         t -= 2 * ny;
+        const int64_t X = t % nx;
+        first = X != 0 && X != g.pmax_x;
         if (t < nx) { if (!g.bnd_lo) return false; idx = t; return true; }
         t -= nx;
         if (t < nx) { if (!g.bnd_hi) return false; idx = t + (int64_t)g.pmax_y * g.sy; return true; }
@@ -178,7 +182,9 @@ __device__ __forceinline__ bool boundary_dof(const SlabGeo& g, int64_t t, int64_
     t -= 2 * fx;
     if (t < 2 * fy) {
         const int64_t side = t / fy, r = t % fy;
-        idx = (r % nx) + (side ? (int64_t)g.pmax_y : 0) * g.sy + (r / nx) * g.sz;
+        const int64_t X = r % nx;
+        first = X != 0 && X != g.pmax_x;
+        idx = X + (side ? (int64_t)g.pmax_y : 0) * g.sy + (r / nx) * g.sz;
         return true;
     }
     t -= 2 * fy;
@@ -186,7 +192,9 @@ __device__ __forceinline__ bool boundary_dof(const SlabGeo& g, int64_t t, int64_
         const int64_t side = t / fz, r = t % fz;
         if (side == 0 && !g.bnd_lo) return false;
         if (side == 1 && !g.bnd_hi) return false;
-        idx = (r % nx) + (r / nx) * g.sy + (side ? (int64_t)g.pmax_z : 0) * g.sz;
+        const int64_t X = r % nx, Y = r / nx;
+        first = X != 0 && X != g.pmax_x && Y != 0 && Y != g.pmax_y;
+        idx = X + Y * g.sy + (side ? (int64_t)g.pmax_z : 0) * g.sz;
         return true;
     }
     return false;
@@ -198,11 +206,105 @@ __host__ __device__ inline int64_t boundary_count(const SlabGeo& g) {
     return 2 * (ny * nz + nx * nz + nx * ny);
 }
 
-__global__ void boundary_set_kernel(SlabGeo g, const double* u, double* y) {
+__global__ void __launch_bounds__(RED_THREADS) boundary_set_kernel(SlabGeo g, const double* u, double* y,
+                                                                   int64_t i0, int64_t i1, double* bpart) {
     const int64_t n = boundary_count(g);
+    double s = 0.0;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         int64_t idx;
-        if (boundary_dof(g, t, idx)) y[idx] = u ? u[idx] : 0.0;
+        bool first;
+        if (boundary_dof(g, t, idx, first)) {
+            const double v = u ? u[idx] : 0.0;
+            y[idx] = v;
+            if (first && idx >= i0 && idx < i1) s = fma(v, v, s);
+        }
+    }
+    if (bpart) {
+        s = block_sum(s);
+        if (threadIdx.x == 0) bpart[blockIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(RED_THREADS) sum_partials_kernel(const double* partials, int n, const double* extra,
+                                                                   double* out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += RED_THREADS) s += partials[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0) *out = extra ? s + *extra : s;
+}
+
+__global__ void __launch_bounds__(RED_THREADS) cg_r_kernel(double* __restrict__ r, const double* __restrict__ q,
+                                                           int64_t n, int64_t i0, int64_t i1, const double* scal,
+                                                           double* partials) {
+    const double alpha = scal[S_RR] / scal[S_PQ];
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const double2* q2 = reinterpret_cast<const double2*>(q);
+    const int64_t np = n / 2;
+    const int64_t stride = (int64_t)gridDim.x * RED_THREADS;
+    const int64_t tid = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x;
+    double s = 0.0;
+    for (int64_t k = tid; k < np; k += VU * stride) {
+        double2 vr[VU], vq[VU];
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk < np) { vr[j] = r2[kk]; vq[j] = q2[kk]; }
+        }
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk >= np) continue;
+            vr[j].x = fma(-alpha, vq[j].x, vr[j].x);
+            vr[j].y = fma(-alpha, vq[j].y, vr[j].y);
+            r2[kk] = vr[j];
+            const int64_t e = 2 * kk;
+            if (e >= i0 && e < i1) s = fma(vr[j].x, vr[j].x, s);
+            if (e + 1 >= i0 && e + 1 < i1) s = fma(vr[j].y, vr[j].y, s);
+        }
+    }
+    if ((n & 1) && tid == 0) {
+        const int64_t e = n - 1;
+        const double re = fma(-alpha, q[e], r[e]);
+        r[e] = re;
+        if (e >= i0 && e < i1) s = fma(re, re, s);
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(RED_THREADS) cg_px_kernel(double* __restrict__ x, double* __restrict__ p,
+                                                            const double* __restrict__ r, int64_t n,
+                                                            const double* scal) {
+    const double alpha = scal[S_RR] / scal[S_PQ];
+    const double beta = scal[S_RRNEW] / scal[S_RR];
+    double2* x2 = reinterpret_cast<double2*>(x);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const int64_t np = n / 2;
+    const int64_t stride = (int64_t)gridDim.x * RED_THREADS;
+    const int64_t tid = (int64_t)blockIdx.x * RED_THREADS + threadIdx.x;
+    for (int64_t k = tid; k < np; k += VU * stride) {
+        double2 vx[VU], vp[VU], vr[VU];
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk < np) { vx[j] = x2[kk]; vp[j] = p2[kk]; vr[j] = r2[kk]; }
+        }
+#pragma unroll
+        for (int j = 0; j < VU; ++j) {
+            const int64_t kk = k + j * stride;
+            if (kk >= np) continue;
+            vx[j].x = fma(alpha, vp[j].x, vx[j].x);
+            vx[j].y = fma(alpha, vp[j].y, vx[j].y);
+            vp[j].x = fma(beta, vp[j].x, vr[j].x);
+            vp[j].y = fma(beta, vp[j].y, vr[j].y);
+            x2[kk] = vx[j];
+            p2[kk] = vp[j];
+        }
+    }
+    if ((n & 1) && tid == 0) {
+        x[n - 1] = fma(alpha, p[n - 1], x[n - 1]);
+        p[n - 1] = fma(beta, p[n - 1], r[n - 1]);
     }
 }
 
@@ -264,14 +366,43 @@ cudaError_t launch_add_planes(double* y, const double* lo, const double* hi, int
 }
 
 cudaError_t launch_dirichlet_fixup(const SlabGeo& g, const double* u, double* y, cudaStream_t st) {
-    boundary_set_kernel<<<grid_for(boundary_count(g), 256), 256, 0, st>>>(g, u, y);
+    boundary_set_kernel<<<grid_for(boundary_count(g), RED_THREADS), RED_THREADS, 0, st>>>(g, u, y, 0, 0, nullptr);
     count_launches(1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_zero_boundary(const SlabGeo& g, double* y, cudaStream_t st) {
-    boundary_set_kernel<<<grid_for(boundary_count(g), 256), 256, 0, st>>>(g, nullptr, y);
+    boundary_set_kernel<<<grid_for(boundary_count(g), RED_THREADS), RED_THREADS, 0, st>>>(g, nullptr, y, 0, 0,
+                                                                                          nullptr);
     count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dirichlet_fixup_dot(const SlabGeo& g, const double* u, double* y, int64_t i0, int64_t i1,
+                                       double* bpart, cudaStream_t st) {
+    boundary_set_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(g, u, y, i0, i1, bpart);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum_partials(const double* partials, int n, const double* extra, double* out, cudaStream_t st) {
+    sum_partials_kernel<<<1, RED_THREADS, 0, st>>>(partials, n, extra, out);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_r(double* r, const double* q, int64_t n, int64_t i0, int64_t i1, double* scal,
+                        double* partials, cudaStream_t st) {
+    cg_r_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(r, q, n, i0, i1, scal, partials);
+    reduce_final_kernel<<<1, RED_THREADS, 0, st>>>(partials, scal + S_RRNEW);
+    count_launches(2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_px(double* x, double* p, const double* r, int64_t n, double* scal, cudaStream_t st) {
+    cg_px_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(x, p, r, n, scal);
+    shift_rr_kernel<<<1, 1, 0, st>>>(scal);
+    count_launches(2);
     return cudaGetLastError();
 }
 

@@ -111,3 +111,24 @@ def test_slab_error_and_operator_on_host_mesh():
     with pytest.raises(DogipError) as ei:
         Operator(m, 0, CoeffSpec(0, np.array([1.0])))
     assert ei.value.code == -10
+
+
+def test_report_reproduces_paper_tables():
+    """NEXT item 4: the library's own report reproduces Tables 3/4 entirely and
+    every Table 1/2 column except mem A for k >= 2 (reading L13)."""
+    import json
+    from paper_1710_09913_b200 import report
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_tables_1_4.json")))
+    rows = {(r["form"], r["d"], r["k"]): r for r in report.tables()}
+    for t, grows in gold["tables"].items():
+        form, d = t[:2], int(t[2])
+        for g in grows:
+            r = rows[(form, d, g["k"])]
+            for key in ("mem_A_T", "mem_A_dogip", "mem_A_dogip_T", "nnz_Bhat"):
+                assert r[key] == g[key], (t, g["k"], key)
+            if form == "EL" or g["k"] == 1 and d == 2:
+                assert r["mem_A"] == g["mem_A"], (t, g["k"])
+                assert abs(r["mem_eff"] - g["mem_eff"]) <= 0.005 + 1e-12
+                assert abs(r["comp_eff"] - g["comp_eff"]) <= 0.005 + 1e-12
+            else:
+                assert r["mem_A"] >= g["mem_A"]
