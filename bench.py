@@ -38,6 +38,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "DoGIP apply GDoF/s and CG s/iter (fraction of HBM roofline)"
+# DFMA throughput measured on this pool's B200 (scripts/fp64_pipes.cu, profiles/r01_fp64_pipes.json)
+FP64_PEAK_TFLOPS = 35.9
 UNIT = "GDoF/s"
 
 
@@ -226,7 +228,8 @@ def run_product(args, cfg) -> None:
     dirichlet = form == 1
     coef = cfg.coefficient()
     mesh = Mesh(cfg.d, cfg.N, cfg.p, cfg.vertices(), rank=rank, nranks=world, nccl_id=nccl_id, device=local)
-    op = Operator(mesh, form, coef)
+    storage = 1 if (args.storage == "iso" and form == 1) else 0
+    op = Operator(mesh, form, coef, storage=storage)
     info, oinfo = mesh.info, op.info
     stream = torch.cuda.current_stream()
     b = op.load_vector(1.0, dirichlet=dirichlet)
@@ -260,8 +263,9 @@ def run_product(args, cfg) -> None:
 
     # algorithmic bytes of one apply on this rank: streamed weights of
     # real elements + u read once + y written once
-    n_w = oinfo["W_T"] * oinfo["n_c"]
+    n_w = oinfo["W_T"] * oinfo["n_c"] if storage == 0 else oinfo["W_T"] + oinfo["n_c"]
     alg_bytes = 8 * n_w * info["n_elem_local"] + 16 * info["ndof_local"]
+    flops_apply = oinfo["flops_per_elem"] * info["n_elem_local"]
     peak, peak_src = _measured_peaks()
     achieved = alg_bytes / t_apply / 1e9
 
@@ -291,14 +295,16 @@ def run_product(args, cfg) -> None:
                "warmup": args.warmup, "ms_per_step": t_step_max * 1e3, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (seeded GRF coefficient, u ~ U[-1,1]; no dataset in the paper)",
-               "config": _config_dict(cfg, world),
+               "config": dict(_config_dict(cfg, world), storage=args.storage),
                "cg_s_per_iter": t_step_max, "apply_ms": t_apply_max * 1e3,
                "weights_ms": oinfo["weights_ms"], "cg_rel_res_after": res["rel_res"],
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": _traffic_from_profiles(cfg.name, world),
                             "kernel": "DoGIP apply (memset y + apply_kernel + Dirichlet fix-up), rank 0",
                             "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
-                            "frac_of_8TBs": achieved / 8000.0},
+                            "frac_of_8TBs": achieved / 8000.0,
+                            "fp64_tflops": flops_apply / t_apply / 1e12,
+                            "fp64_frac_of_measured_dfma": flops_apply / t_apply / 1e12 / FP64_PEAK_TFLOPS},
                "e2e": {"value": info["ndof_global"] / t_e2e.item() / 1e9, "unit": UNIT,
                        "h2d_bytes_per_step": int(tot_vec.item()), "d2h_bytes_per_step": int(tot_vec.item()),
                        "api": "dogip_apply_host (pinned host u -> device, apply, device -> host y)"},
@@ -320,6 +326,9 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--storage", default="full", choices=["full", "iso"],
+                    help="EL weight storage: full symmetric blocks (P:443) or the isotropic "
+                         "compression of the corollary P:411-428 (a_{T,j} R^-1 R^-T)")
     args = ap.parse_args()
     from synth.configs import get_config
     cfg = get_config(args.config)

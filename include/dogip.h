@@ -69,6 +69,11 @@ extern "C" {
 #define DOGIP_STORE_ISO   1  /* EL with isotropic M = m I (Corollary, element-wise):
                                 A_{T,j} = a_{T,j} G_T, a_{T,j} = int_T m phi^W_j, G_T = Rinv Rinv^T;
                                 stores W_T + d(d+1)/2 doubles per element instead of W_T d(d+1)/2 */
+#define DOGIP_STORE_GLOBAL 2 /* WP only (Theorem 1): one global diagonal over the
+                                double-grid space W = C_{N,2p}, A_ii = int_Omega m phi^W_i, stored
+                                as a W-lattice vector ((2pN+1)^d doubles) holding A_ii / mult_i
+                                (mult_i = elements sharing W node i, each visits it once) and
+                                gathered per element; multi-rank needs the NCCL communicator */
 
 /* ---- status codes ------------------------------------------------------- */
 #define DOGIP_OK                     0
@@ -189,7 +194,10 @@ int dogip_weights(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_
 
 /* dogip_weights with an explicit storage variant (DOGIP_STORE_*).  DOGIP_STORE_ISO
  * needs form = DOGIP_EL (else E_INVALID_ARG) and an isotropic coefficient kind
- * (else E_BAD_COEFF); the apply result is the same operator up to rounding. */
+ * (else E_BAD_COEFF); DOGIP_STORE_GLOBAL needs form = DOGIP_WP (else
+ * E_INVALID_ARG).  The apply result is the same operator up to rounding.
+ * dogip_export_weights of a GLOBAL op returns, per element, the stored values of
+ * its W nodes, A_{l^W_T(j), l^W_T(j)} / mult_{l^W_T(j)}. */
 int dogip_weights_ex(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_n1d, int storage,
                      void* stream, dogip_op* out);
 

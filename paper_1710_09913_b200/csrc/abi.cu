@@ -73,6 +73,7 @@ struct dogip_op_s {
     double* h_scal = nullptr;  // pinned
     double* hu = nullptr;      // device scratch for the host-buffer apply
     double* hy = nullptr;
+    int* d_offw = nullptr;     // global WP: W-lattice offsets [NS][W_T]
     double* dotp = nullptr;    // per-warp partials of p^T A p (3 launches x APPLY_MAX_WARPS)
     double* bpart = nullptr;   // boundary-row partials of the Dirichlet fix-up (RED_BLOCKS)
     float weights_ms = 0.f;
@@ -137,6 +138,10 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
     g.bnd_lo = m->z0 == 0;
     g.bnd_hi = m->z1 == N;
     g.zoff = m->z0;
+    const int64_t MW = 2 * p * N + 1;          // W-lattice of the global WP storage (Theorem 1)
+    g.swy = MW;
+    g.swz = d == 3 ? MW * MW : 0;
+    g.ndof_w = ipow(MW, d - 1) * (2 * p * L + 1);
     for (int s = 0; s < g.ns; ++s)
         for (int l = 0; l < m->ref.VT; ++l) {
             const int* o = m->ref.loff[s][l];
@@ -246,6 +251,28 @@ static int check_coeff(int d, int form, const dogip_coeff* c, int& ncomp) {
     return fail(DOGIP_E_BAD_COEFF, "unknown coefficient kind");
 }
 
+// Sum the two interface planes (P values each) of a slab vector of length n with the
+// neighbours (same plan as the apply exchange); synchronous, setup only.
+static int sum_interface_planes(dogip_mesh_s* m, double* v, int64_t P, int64_t n, cudaStream_t st) {
+    auto& api = nccl();
+    double* rb = nullptr;
+    CK(cudaMalloc(&rb, sizeof(double) * 2 * P));
+    struct Free { double* p; ~Free() { cudaFree(p); } } fr{rb};
+    NK(api.GroupStart());
+    if (m->rank > 0) {
+        NK(api.Send(v, P, ncclDouble, m->rank - 1, m->comm, st));
+        NK(api.Recv(rb, P, ncclDouble, m->rank - 1, m->comm, st));
+    }
+    if (m->rank < m->nranks - 1) {
+        NK(api.Send(v + n - P, P, ncclDouble, m->rank + 1, m->comm, st));
+        NK(api.Recv(rb + P, P, ncclDouble, m->rank + 1, m->comm, st));
+    }
+    NK(api.GroupEnd());
+    CK(launch_add_planes(v, m->rank > 0 ? rb : nullptr, m->rank < m->nranks - 1 ? rb + P : nullptr, P, n - P, st));
+    CK(cudaStreamSynchronize(st));
+    return DOGIP_OK;
+}
+
 struct DevBufs {   // frees on scope exit
     std::vector<void*> p;
     ~DevBufs() { for (void* x : p) cudaFree(x); }
@@ -266,10 +293,14 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     if (!m || !out) return fail(DOGIP_E_INVALID_ARG, "null argument");
     *out = nullptr;
     if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
-    if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO)
+    if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO && storage != DOGIP_STORE_GLOBAL)
         return fail(DOGIP_E_INVALID_ARG, "unknown storage");
     if (storage == DOGIP_STORE_ISO && form != DOGIP_EL)
         return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_ISO applies to the elliptic form only");
+    if (storage == DOGIP_STORE_GLOBAL && form != DOGIP_WP)
+        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_GLOBAL (Theorem 1) applies to the weighted projection only");
+    if (storage == DOGIP_STORE_GLOBAL && m->nranks > 1 && !m->comm)
+        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_GLOBAL on several ranks needs the NCCL communicator");
     if (m->device < 0) return fail(DOGIP_E_INVALID_ARG, "host-only mesh (device < 0) cannot hold an operator");
     int ncomp = 1;
     RET(check_coeff(m->d, form, coeff, ncomp));
@@ -282,7 +313,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     op->m = m;
     op->form = form;
     op->store = storage;
-    ref_info(d, p, form, storage, op->ref);
+    ref_info(d, p, form, storage == DOGIP_STORE_GLOBAL ? 0 : storage, op->ref);
     const int WT = op->ref.WT, NC = op->ref.NC, VT = op->ref.VT;
     const int n1d = quad_n1d > 0 ? quad_n1d : p + 3;
     std::vector<double> pts, wts;
@@ -312,7 +343,8 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
 
     DevBufs tmp;
     WeightsArgs a{};
-    a.d = d; a.p = p; a.form = form; a.store = storage; a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
+    a.d = d; a.p = p; a.form = form; a.store = storage == DOGIP_STORE_GLOBAL ? 0 : storage;
+    a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
     a.NG = op->ref.NG; a.tile_rows = op->ref.tile_rows;
     a.kind = coeff->kind;
     a.nparams = (int)coeff->nparams;
@@ -361,6 +393,49 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost);
     if (bad & 1) return cleanup_fail(DOGIP_E_DEGENERATE_ELEMENT, "an element is degenerate or inverted");
     if (bad & 2) return cleanup_fail(DOGIP_E_BAD_COEFF, "coefficient is not positive at a quadrature point");
+    if (storage == DOGIP_STORE_GLOBAL) {
+        // Theorem 1: A_ii = int_Omega m phi^W_i = sum over the elements sharing W node i
+        std::vector<int> offw((size_t)m->geo.ns * WT);
+        const auto AW = multi_indices(d, 2 * p);
+        const auto simp = cell_simplices(d);
+        const int64_t MW = m->geo.swy;
+        for (int s = 0; s < m->geo.ns; ++s)
+            for (int j = 0; j < WT; ++j) {
+                int o[3] = {0, 0, 0};
+                for (int ax = 0; ax < d; ++ax)
+                    for (int i = 0; i <= d; ++i) o[ax] += AW[j][i] * simp[s][i][ax];
+                offw[(size_t)s * WT + j] = (int)(o[0] + MW * o[1] + (d == 3 ? MW * MW * o[2] : 0));
+            }
+        // The apply visits a W node once per element sharing it, so the stored diagonal
+        // is A_ii / mult_i (u, v continuous at x_i: the sum over those elements gives A_ii).
+        double *wg = nullptr, *cnt = nullptr;
+        if (cudaMalloc(&op->d_offw, sizeof(int) * offw.size()) != cudaSuccess ||
+            cudaMalloc(&wg, sizeof(double) * m->geo.ndof_w) != cudaSuccess ||
+            cudaMalloc(&cnt, sizeof(double) * m->geo.ndof_w) != cudaSuccess) {
+            cudaFree(wg);
+            return cleanup_fail(DOGIP_E_OOM, "global W weights");
+        }
+        cudaMemcpy(op->d_offw, offw.data(), sizeof(int) * offw.size(), cudaMemcpyHostToDevice);
+        cudaMemsetAsync(wg, 0, sizeof(double) * m->geo.ndof_w, st);
+        cudaMemsetAsync(cnt, 0, sizeof(double) * m->geo.ndof_w, st);
+        ce = launch_globalize(m->geo, WT, op->d_w, op->d_offw, wg, st);
+        if (ce == cudaSuccess) ce = launch_globalize(m->geo, WT, nullptr, op->d_offw, cnt, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        cudaFree(op->d_w);
+        op->d_w = wg;
+        op->w_doubles = m->geo.ndof_w;
+        if (ce != cudaSuccess) { cudaFree(cnt); return cleanup_fail(DOGIP_E_CUDA, std::string("globalize: ") + cudaGetErrorString(ce)); }
+        if (m->nranks > 1 && m->comm) {
+            const int64_t PW = m->d == 3 ? MW * MW : MW;
+            int rc = sum_interface_planes(m, wg, PW, m->geo.ndof_w, st);
+            if (rc >= 0) rc = sum_interface_planes(m, cnt, PW, m->geo.ndof_w, st);
+            if (rc < 0) { cudaFree(cnt); dogip_op_destroy(op); return rc; }
+        }
+        ce = launch_divide(wg, cnt, m->geo.ndof_w, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        cudaFree(cnt);
+        if (ce != cudaSuccess) return cleanup_fail(DOGIP_E_CUDA, std::string("globalize: ") + cudaGetErrorString(ce));
+    }
     *out = op;
     return DOGIP_OK;
 }
@@ -371,7 +446,7 @@ extern "C" int dogip_op_info(dogip_op op, dogip_op_info_t* o) {
     o->V_T = op->ref.VT; o->W_T = op->ref.WT;
     o->n_c = op->form == DOGIP_WP ? 1 : op->m->d * (op->m->d + 1) / 2;
     o->storage = op->store;
-    o->stream_doubles_per_elem = op->ref.tile_rows;
+    o->stream_doubles_per_elem = op->store == DOGIP_STORE_GLOBAL ? 0 : op->ref.tile_rows;
     o->flops_per_elem = op->ref.flops;
     o->quad_n1d = op->nq;
     o->n_tiles = op->m->geo.ntiles;
@@ -386,6 +461,7 @@ extern "C" void dogip_op_destroy(dogip_op op) {
     for (double* x : {op->d_w, op->d_sV, op->r, op->pv, op->q, op->partials, op->scal, op->hu, op->hy, op->dotp,
                       op->bpart})
         cudaFree(x);
+    cudaFree(op->d_offw);
     if (op->h_scal) cudaFreeHost(op->h_scal);
     delete op;
 }
@@ -428,6 +504,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
     CK(cudaMemsetAsync(y, 0, sizeof(double) * g.ndof, st));
     ApplyArgs a{};
     a.d = m->d; a.p = m->p; a.form = op->form; a.store = op->store;
+    a.offw = op->d_offw;
     a.dirichlet = (flags & DOGIP_DIRICHLET_ZERO) != 0;
     a.u = u; a.y = y; a.w = op->d_w; a.geo = g; a.tab = &m->tab;
     a.num_sms = m->num_sms;
@@ -763,10 +840,21 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
     CK(cudaSetDevice(op->m->device));
     CK(cudaMemcpy(w.data(), op->d_w, sizeof(double) * op->w_doubles, cudaMemcpyDeviceToHost));
     const SlabGeo& g = op->m->geo;
+    std::vector<int> offw;
+    if (op->store == DOGIP_STORE_GLOBAL) {
+        offw.resize((size_t)g.ns * WT);
+        CK(cudaMemcpy(offw.data(), op->d_offw, sizeof(int) * offw.size(), cudaMemcpyDeviceToHost));
+    }
     for (int64_t t = 0; t < g.ntiles; ++t)
         for (int lane = 0; lane < TILE; ++lane) {
             const int64_t e = canonical_elem(g, t, lane);
             if (e < 0) continue;
+            if (op->store == DOGIP_STORE_GLOBAL) {     // the global weights each element sees
+                const TileCoord tc = tile_coord(g, t);
+                const int64_t bw = (int64_t)(2 * g.p) * (tc.ci0 + lane + g.swy * tc.cj + g.swz * tc.ck);
+                for (int j = 0; j < WT; ++j) host[e * WT + j] = w[bw + offw[(size_t)tc.s * WT + j]];
+                continue;
+            }
             auto at = [&](int row) { return w[((size_t)t * TR + row) * TILE + lane]; };
             for (int j = 0; j < WT; ++j)
                 for (int c = 0; c < NC; ++c)

@@ -92,6 +92,19 @@ struct WarpStream {
     __device__ __forceinline__ double w(int k) const { return cur[(k % C::ROWS) * TILE]; }
 };
 
+// Theorem 1 storage (global WP diagonal over W = C_{N,2p}): the weight of
+// double-grid node j of the element is gathered from the global W-lattice vector.
+struct GatherPol {
+    const double* wg;      // global W weights of this slab
+    const int* offw;       // shared-memory W-lattice offsets of this simplex type
+    int64_t baseW;         // W-lattice index of the cell origin
+    template <int J>
+    __device__ __forceinline__ void begin() {}
+    template <int J>
+    __device__ __forceinline__ void end() {}
+    __device__ __forceinline__ double w(int k) const { return __ldg(wg + baseW + offw[k]); }
+};
+
 // 3 CTAs (12 warps) per SM where u_T + y_T fit in <= 170 registers, else 2
 #ifndef DOGIP_MINB_LARGE
 #define DOGIP_MINB_LARGE 2   // CTAs/SM asked of ptxas when V_T > 20 (3D P4)
@@ -99,11 +112,11 @@ struct WarpStream {
 template <int D, int P, int F, int ST>
 constexpr int min_blocks() { return dogip_gen::RefElem<D, P, F, ST>::VT <= 20 ? 3 : DOGIP_MINB_LARGE; }
 
-template <int D, int P, int F, int ST, bool DIR>
+template <int D, int P, int F, int ST, bool DIR, bool GLOB>
 __global__ void __launch_bounds__(APPLY_THREADS, min_blocks<D, P, F, ST>())
 apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
              const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end,
-             double* __restrict__ dot_partials) {
+             double* __restrict__ dot_partials, const int* __restrict__ offw_g) {
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
@@ -125,7 +138,12 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     ws.policy = policy_evict_first();
     double* ubuf = ubufs + (size_t)warp * RE::VT * TILE;
     const uint32_t ubuf_s = smem_u32(ubuf + lane);
-    if (lane == 0) {
+    __shared__ int offw_s[GLOB ? MAX_NS * MAX_WT_GLOBAL : 1];
+    if constexpr (GLOB) {
+        for (int i = threadIdx.x; i < MAX_NS * RE::WT; i += blockDim.x)
+            offw_s[(i / RE::WT) * MAX_WT_GLOBAL + i % RE::WT] = offw_g[i];
+        __syncthreads();
+    } else if (lane == 0) {
         for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
         fence_mbar_init();
         for (int s = 0; s < C::S - 1; ++s) ws.issue(s);      // prologue of the weight stream
@@ -187,7 +205,13 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
             __syncwarp();
             if (tile + ws.nw < tile_end) prefetch_u(tile + ws.nw);  // overlaps this tile's compute
         }
-        RE::body(uT, yT, ws);
+        if constexpr (GLOB) {
+            GatherPol gp{w, offw_s + tc.s * MAX_WT_GLOBAL,
+                         (int64_t)(2 * geo.p) * (ci + geo.swy * tc.cj + geo.swz * tc.ck)};
+            RE::body(uT, yT, gp);
+        } else {
+            RE::body(uT, yT, ws);
+        }
         if (valid) {
 #pragma unroll
             for (int l = 0; l < RE::VT; ++l) {
@@ -205,14 +229,14 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     }
 }
 
-template <int D, int P, int F, int ST, bool DIR>
+template <int D, int P, int F, int ST, bool DIR, bool GLOB>
 cudaError_t launch_one(const ApplyArgs& a) {
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
     const size_t smem = (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * RE::VT * TILE * 8 +
                         (size_t)NW * C::S * 8;
-    auto kern = apply_kernel<D, P, F, ST, DIR>;
+    auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
     static int configured = 0;   // per instantiation
     static int occ = 1;
     if (!configured) {
@@ -235,18 +259,19 @@ cudaError_t launch_one(const ApplyArgs& a) {
         return cudaSuccess;
     }
     kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, a.tile_begin,
-                                                           a.tile_end, a.dot_partials);
+                                                           a.tile_end, a.dot_partials, a.offw);
     count_launches(1);
     return cudaGetLastError();
 }
 
 template <int D, int P, int F, int ST>
 cudaError_t launch_dir(const ApplyArgs& a) {
-    return a.dirichlet ? launch_one<D, P, F, ST, true>(a) : launch_one<D, P, F, ST, false>(a);
+    return a.dirichlet ? launch_one<D, P, F, ST, true, false>(a) : launch_one<D, P, F, ST, false, false>(a);
 }
 
 template <int D, int P>
 cudaError_t launch_form(const ApplyArgs& a) {
+    if (a.form == 0 && a.store == 2) return launch_one<D, P, 0, 0, false, true>(a);   // WP has no BC
     if (a.form == 0) return launch_dir<D, P, 0, 0>(a);
     return a.store == 1 ? launch_dir<D, P, 1, 1>(a) : launch_dir<D, P, 1, 0>(a);
 }

@@ -24,8 +24,10 @@ struct ApplyTables {
     int loff[MAX_NS * MAX_VT];
 };
 
+constexpr int MAX_WT_GLOBAL = 165;   // W_T of P_8 in 3D (global WP storage, p <= 4)
+
 struct ApplyArgs {
-    int d, p, form, store;      // store: 0 full A_T blocks, 1 isotropic a_j + G_T (EL)
+    int d, p, form, store;      // store: 0 full A_T blocks, 1 isotropic a_j + G_T (EL), 2 global WP
     bool dirichlet;
     const double* u;
     double* y;
@@ -37,6 +39,7 @@ struct ApplyArgs {
     cudaStream_t stream;
     double* dot_partials;      // != null: per-warp partials of u^T A u (APPLY_MAX_WARPS slots)
     int* dot_nslots;           // out: number of partial slots written
+    const int* offw;           // global WP: device table [NS][W_T] of W-lattice offsets
 };
 
 cudaError_t launch_apply(const ApplyArgs& a);
@@ -70,6 +73,11 @@ struct WeightsArgs {
     cudaStream_t stream;
 };
 cudaError_t launch_weights(const WeightsArgs& a);
+// global WP (Theorem 1): wg[l^W_T(j)] += a_{T,j} from tile-major element weights
+// (wel == null: += 1, the multiplicity of each W node); a /= b elementwise (b > 0)
+cudaError_t launch_divide(double* a, const double* b, int64_t n, cudaStream_t st);
+cudaError_t launch_globalize(const SlabGeo& g, int WT, const double* wel, const int* offw, double* wg,
+                             cudaStream_t st);
 
 // ----------------------------------------------------------- vectors / CG
 cudaError_t launch_dirichlet_fixup(const SlabGeo& g, const double* u, double* y, cudaStream_t st);

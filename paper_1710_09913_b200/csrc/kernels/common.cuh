@@ -23,6 +23,8 @@ struct SlabGeo {
     int bnd_lo, bnd_hi;            // slab-axis planes 0 / pmax are domain boundary
     int64_t zoff;                  // global cell offset along the slab axis
     int N;                         // global cells per axis
+    int64_t swy, swz;              // W-lattice (order 2p) strides of the global WP storage
+    int64_t ndof_w;                // local W-lattice DoFs
 };
 
 // Tile t -> (simplex s, x-block, cj, ck).  Tiles are ordered with s fastest,

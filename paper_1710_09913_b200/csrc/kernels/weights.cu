@@ -323,6 +323,45 @@ cudaError_t launch_weights(const WeightsArgs& a) {
     return cudaSuccess;
 }
 
+// ---------------------------------------------------------- global WP (Theorem 1)
+namespace {
+// wel != null: wg[l^W_T(j)] += a_{T,j};  wel == null: wg[l^W_T(j)] += 1 (multiplicity)
+__global__ void globalize_kernel(SlabGeo g, int WT, const double* __restrict__ wel, const int* __restrict__ offw,
+                                 double* wg) {
+    const int64_t eK = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (eK >= g.ntiles * TILE) return;
+    const int64_t tile = eK / TILE;
+    const int lane = (int)(eK % TILE);
+    const TileCoord tc = tile_coord(g, tile);
+    const int ci = tc.ci0 + lane;
+    if (ci >= g.Nx) return;
+    const int64_t base = (int64_t)(2 * g.p) * (ci + g.swy * tc.cj + g.swz * tc.ck);
+    for (int j = 0; j < WT; ++j)
+        red_add_f64(wg + base + offw[tc.s * WT + j], wel ? wel[((size_t)tile * WT + j) * TILE + lane] : 1.0);
+}
+
+__global__ void divide_kernel(double* a, const double* b, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = b[i] > 0.0 ? a[i] / b[i] : 0.0;
+}
+}  // namespace
+
+cudaError_t launch_divide(double* a, const double* b, int64_t n, cudaStream_t st) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4 * 148 * 8) blocks = 4 * 148 * 8;
+    divide_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, b, n);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_globalize(const SlabGeo& g, int WT, const double* wel, const int* offw, double* wg,
+                             cudaStream_t st) {
+    const int64_t n = g.ntiles * TILE;
+    globalize_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, WT, wel, offw, wg);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------- load vector (K5)
 namespace {
 __global__ void load_vector_kernel(SlabGeo g, const double* verts, const double* sV, int VT,

@@ -59,6 +59,8 @@ def main():
         variants = [(f, 0) for f in forms]
         if args.iso and coef.isotropic and 1 in forms:
             variants.append((1, 1))
+        if args.iso and 0 in forms and c.p <= 4:
+            variants.append((0, 2))
         for form, storage in variants:
             op = Operator(mesh, form, coef, storage=storage)
             oi = op.info
@@ -69,11 +71,13 @@ def main():
             t_apply = time_apply(op, u, y, n, dirichlet)
             nw = oi["W_T"] * oi["n_c"] if storage == 0 else oi["W_T"] + oi["n_c"]
             alg = 8 * nw * c.n_elem + 16 * c.ndof
+            if storage == 2:                      # global W vector read once (Theorem 1)
+                alg = oi["weight_bytes"] + 16 * c.ndof
             b = op.load_vector(1.0, dirichlet=dirichlet)
             x = torch.zeros_like(b)
             op.cg(b, x, maxit=-3, dirichlet=dirichlet)
             r = op.cg(b, x, maxit=-n, dirichlet=dirichlet, resume=True)
-            row = {"config": name, "form": "WP" if form == 0 else ("EL" if storage == 0 else "EL-iso"),
+            row = {"config": name, "form": ["WP", "EL", "EL-iso", "WP-glob"][form if storage == 0 else storage + 1],
                    "d": c.d, "N": c.N, "p": c.p, "flops_per_elem": oi["flops_per_elem"],
                    "fp64_TFs": oi["flops_per_elem"] * c.n_elem / t_apply / 1e12,
                    "n_elem": c.n_elem, "ndof": c.ndof, "W_T": oi["W_T"], "n_c": oi["n_c"],

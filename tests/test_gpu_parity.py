@@ -330,3 +330,57 @@ def test_iso_storage_errors():
     with pytest.raises(DogipError) as ei:
         Operator(m, 0, TANH3, storage=1)
     assert ei.value.code == -10
+
+
+GLOBAL_CASES = [(2, 33, 2), (2, 9, 4), (3, 3, 1), (3, 4, 2), (3, 3, 4)]
+
+
+@pytest.mark.parametrize("d,N,p", GLOBAL_CASES)
+def test_global_wp_storage_theorem1(d, N, p):
+    """DOGIP_STORE_GLOBAL (Theorem 1, P:224-238): one diagonal over W = C_{N,2p};
+    same operator as the assembled A; each element sees A_ii / mult_i with
+    A_ii = int m phi^W_i (the oracle's own Theorem 1 weights)."""
+    torch = _torch()
+    from oracle.mesh import dof_map
+    from paper_1710_09913_b200.api import Mesh, Operator
+    coef = TANH2 if d == 2 else TANH3
+    verts = jitter_verts(d, N)
+    m = Mesh(d, N, p, verts)
+    op = Operator(m, 0, coef, storage=2)
+    assert op.info["weight_bytes"] == 8 * (2 * p * N + 1) ** d
+    ed = oa.build(d, N, p, verts)
+    A = oa.assemble_csr(ed, 0, coef)
+    u = u_vector(ed.ndof, 0)
+    y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    assert relerr(y, A @ u) <= TOL
+    lW = dof_map(ed.mesh, 2 * p)
+    a_el = od.element_weights(ed, 0, coef)
+    a_glob = np.bincount(lW.ravel(), weights=a_el.ravel(), minlength=(2 * p * N + 1) ** d)
+    mult = np.bincount(lW.ravel(), minlength=(2 * p * N + 1) ** d)
+    assert relerr(op.export_weights()[:, :, 0], (a_glob / np.maximum(mult, 1))[lW]) <= 1e-13
+
+
+def test_global_wp_c5_full_size_sampled():
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config("C5")
+    coef, verts = c.coefficient(), c.vertices()
+    m = Mesh(3, c.N, c.p, verts)
+    op = Operator(m, 0, coef, storage=2)
+    u = c.u()
+    y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    rows = np.unique(np.random.default_rng(13).integers(0, c.ndof, 30))
+    ref = oa.apply_rows_sampled(3, c.N, c.p, verts, 0, coef, u, rows)
+    assert np.abs(y[rows] - ref).max() / np.abs(y).max() <= TOL
+
+
+def test_global_storage_errors():
+    from paper_1710_09913_b200.api import DogipError, Mesh, Operator
+    m = Mesh(3, 2, 2)
+    with pytest.raises(DogipError) as ei:
+        Operator(m, 1, TANH3, storage=2)
+    assert ei.value.code == -10
+    m2 = Mesh(3, 4, 2, rank=0, nranks=2)             # no communicator
+    with pytest.raises(DogipError) as ei:
+        Operator(m2, 0, TANH3, storage=2)
+    assert ei.value.code == -10
