@@ -147,7 +147,19 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
             const int* o = m->ref.loff[s][l];
             m->tab.off[s * MAX_VT + l] = (int)(o[0] + M * o[1] + (d == 3 ? M * M * o[2] : 0));
             m->tab.loff[s * MAX_VT + l] = o[0] | (o[1] << 8) | (o[2] << 16);
+            for (int ax = 0; ax < d; ++ax) {
+                if (o[ax] == 0) m->tab.fmask[s][2 * ax] |= 1ull << l;
+                if (o[ax] == p) m->tab.fmask[s][2 * ax + 1] |= 1ull << l;
+            }
         }
+    {
+        const auto simp = cell_simplices(d);
+        for (int s = 0; s < g.ns; ++s)
+            for (int i = 1; i <= d; ++i) {
+                const auto& v = simp[s][i];
+                m->tab.vstr[s][i - 1] = (int)(v[0] + M * v[1] + (d == 3 ? M * M * v[2] : 0));
+            }
+    }
     if (device < 0) {   // host-only mesh: partition / numbering introspection, no device work
         *out = m;
         return DOGIP_OK;

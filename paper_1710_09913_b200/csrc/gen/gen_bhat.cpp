@@ -118,6 +118,15 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
         std::fprintf(f, "}");
     }
     std::fprintf(f, "};\n");
+    // ALPHA[l][i-1] = alpha_i of local DoF l (i = 1..d).  Every simplex of the cell has
+    // v_0 = cell origin, so LOFF[s][l] = sum_i ALPHA[l][i-1] * v_i(s): the kernel forms
+    // gather offsets from d per-tile vertex strides instead of a per-DoF table.
+    for (auto& sv : simp)
+        if (sv[0][0] || sv[0][1] || sv[0][2]) { std::fprintf(stderr, "v_0 must be the cell origin\n"); std::exit(1); }
+    std::fprintf(f, "    static constexpr signed char ALPHA[%d][3] = {", VT);
+    for (int l = 0; l < VT; ++l)
+        std::fprintf(f, "%s{%d,%d,%d}", l ? "," : "", A[l][1], A[l][2], d == 3 ? A[l][3] : 0);
+    std::fprintf(f, "};\n");
     // row of node j's first weight, and its chunk
     auto row = [&](int j) { return NG + j * NC; };
     auto chunk = [&](int j) { return row(j) / ROWS; };

@@ -5,8 +5,7 @@
 //                                              Theorem 4 eq:ep_dogip_mul P:439)
 // Mapping:
 //  * one warp = one 32-element tile = 32 consecutive cells along x with the same
-//    simplex type s; one lane = one element (gather offsets are warp-uniform and
-//    read from the kernel-parameter bank);
+//    simplex type s; one lane = one element;
 //  * the per-element work g = Bhat u_T, h = A_T g, y_T += Bhat^T h is the
 //    generated straight-line, sparsity- and +-1-aware FP64 code of
 //    generated/bhat_gen.cuh, node by node, so only u_T and y_T sit in registers;
@@ -14,11 +13,15 @@
 //    by each warp through its own S-stage shared-memory ring with 1D bulk
 //    copies (cp.async.bulk, the TMA engine) that complete on mbarriers; the
 //    stream runs ahead across tile boundaries, so HBM requests stay in flight
-//    independently of register pressure;
-//  * u_T is gathered with read-only loads (neighbouring lanes share cache
-//    lines), y_T is scattered with fire-and-forget red.global.add.f64 (y must
-//    be zeroed first); DIRICHLET zeroes boundary DoFs of u_T and skips their
-//    scatter (the boundary rows are fixed by dirichlet_fixup).
+//    independently of register pressure.  Chunk boundaries are compile-time
+//    (node rows), so the refill address is one add off the tile pointer;
+//  * gather/scatter offsets are formed in registers: every simplex of the cell
+//    has v_0 = cell origin, so off(l) = sum_i alpha_i(l) v_i(s) with compile-time
+//    alpha and d per-tile vertex strides (no per-DoF table loads);
+//  * the next tile's u_T is gathered (read-only loads) before this tile's y_T is
+//    scattered with fire-and-forget red.global.add.f64 (y zeroed first), so the
+//    gather latency overlaps the scatter; DIRICHLET zeroes boundary DoFs of u_T
+//    and skips their scatter (the boundary rows are fixed by dirichlet_fixup).
 #include <cuda_runtime.h>
 
 #ifdef DOGIP_GEN_HEADER
@@ -26,24 +29,47 @@
 #else
 #include "../generated/bhat_gen.cuh"
 #endif
-#ifndef DOGIP_UPREFETCH
-// cp.async (LDGSTS) prefetch of the next tile's u_T into shared memory.  Measured
-// slower than direct read-only gathers on B200 (profiles/r01_ab_variants.log), off.
-#define DOGIP_UPREFETCH 0
-#endif
 #include "apply.cuh"
 #include "common.cuh"
+
+#ifndef DOGIP_STAGES
+#define DOGIP_STAGES 4          // ring stages per warp
+#endif
+#ifndef DOGIP_ROWS_3CTA
+#define DOGIP_ROWS_3CTA 18      // max rows per chunk when 3 CTAs share an SM
+#endif
+#ifndef DOGIP_ROWS_2CTA
+#define DOGIP_ROWS_2CTA 24      // ... when 2 CTAs share an SM
+#endif
 
 namespace dogip {
 
 namespace {
 
+// 3 CTAs (12 warps) per SM where u_T + y_T fit in <= 170 registers, else 2
+#ifndef DOGIP_MINB_LARGE
+#define DOGIP_MINB_LARGE 2   // CTAs/SM asked of ptxas when V_T > 20 (3D P4)
+#endif
+template <class RE>
+constexpr int min_blocks() { return RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE; }
+
+// Balanced chunks of whole nodes: NCH = ceil(TILE_ROWS / ROWS_MAX) chunks of ROWS rows
+// (a multiple of NC, so a node's NC rows never straddle two chunks; the NG leading
+// rows of the iso storage sit in chunk 0), the last chunk shorter.
 template <class RE>
 struct Chunking {
-    static constexpr int ROWS = RE::ROWS;                                 // rows per streamed chunk
-    static constexpr int TILE_ROWS = RE::TILE_ROWS;                       // rows per tile
+    static constexpr int S = DOGIP_STAGES;
+    static constexpr int TILE_ROWS = RE::TILE_ROWS;
+    static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA : DOGIP_ROWS_2CTA;
+    static constexpr int ROWS_MAX = (ROWS_MAX0 / RE::NC) * RE::NC;
+    static constexpr int NCH0 = (TILE_ROWS + ROWS_MAX - 1) / ROWS_MAX;
+    static constexpr int ROWS_B = (TILE_ROWS + NCH0 - 1) / NCH0;
+    static constexpr int ROWS1 = ((ROWS_B + RE::NC - 1) / RE::NC) * RE::NC;
+    static constexpr int ROWS = ROWS1 < RE::NG + RE::NC ? RE::NG + RE::NC : ROWS1;
     static constexpr int NCH = (TILE_ROWS + ROWS - 1) / ROWS;             // chunks per tile
-    static constexpr int S = 4;                                           // ring stages per warp
+    static constexpr int LAST = TILE_ROWS - (NCH - 1) * ROWS;              // rows of the last chunk
+    static constexpr int64_t TILE_DBL = (int64_t)TILE_ROWS * TILE;         // doubles per tile
+    static_assert(RE::NG == 0 || RE::NG <= ROWS, "iso G rows must sit in chunk 0");
 };
 
 template <class RE>
@@ -52,44 +78,56 @@ struct WarpStream {
     double* ring;          // this warp's ring in shared memory
     uint32_t bar0;         // smem address of this warp's S mbarriers
     int lane;
-    const double* wbase;   // global weights (tile-major)
-    int64_t gw, nw, tile_end;
-    int64_t g_cons;        // next chunk (warp-global sequence) to consume
+    const double* tptr;    // weights of the tile being consumed
+    int64_t tstride;       // doubles between this warp's consecutive tiles
+    int64_t tiles_left;    // this warp's tiles from the current one on
+    uint32_t cons;         // chunks consumed so far (stage = cons % S, parity = cons / S)
     const double* cur;     // current stage + lane
     uint64_t policy;
 
-    __device__ __forceinline__ void issue(int64_t gg) const {   // lane 0 only
-        const int64_t it = gg / C::NCH;
-        const int c = (int)(gg - it * C::NCH);
-        const int64_t tile = gw + it * nw;
-        if (tile >= tile_end) return;
-        const int rows = (c == C::NCH - 1) ? C::TILE_ROWS - c * C::ROWS : C::ROWS;
-        const uint32_t bytes = (uint32_t)rows * TILE * 8u;
-        const int st = (int)(gg % C::S);
-        const uint32_t bar = bar0 + 8u * st;
+    // chunk-sequence number g (relative: K tiles ahead, chunk c) -> stage g % S
+    template <int K, int CI>
+    __device__ __forceinline__ void issue(uint32_t stage) const {   // lane 0 only
+        if (K >= tiles_left) return;
+        constexpr int rows = (CI == C::NCH - 1) ? C::LAST : C::ROWS;
+        constexpr uint32_t bytes = (uint32_t)rows * TILE * 8u;
+        const uint32_t bar = bar0 + 8u * stage;
         mbar_expect_tx(bar, bytes);
-        bulk_g2s_evict_first(smem_u32(ring + (size_t)st * C::ROWS * TILE),
-                             wbase + ((size_t)tile * C::TILE_ROWS + (size_t)c * C::ROWS) * TILE,
-                             bytes, bar, policy);
+        bulk_g2s_evict_first(smem_u32(ring + (size_t)stage * C::ROWS * TILE),
+                             tptr + K * tstride + (int64_t)CI * C::ROWS * TILE, bytes, bar, policy);
     }
+    template <int G>
+    __device__ __forceinline__ void prologue_one() {
+        if constexpr (G < C::S - 1) {
+            issue<G / C::NCH, G % C::NCH>((uint32_t)G);
+            prologue_one<G + 1>();
+        }
+    }
+    __device__ __forceinline__ void prologue() { prologue_one<0>(); }
     // node J's weights start a new chunk (node 0 also covers the NG leading rows)
     template <int J>
     __device__ __forceinline__ void begin() {
-        if constexpr (J == 0 || RE::row_of(J) / C::ROWS != RE::row_of(J - 1) / C::ROWS) {
+        constexpr int c_cur = RE::row_of(J) / C::ROWS;
+        if constexpr (J == 0 || c_cur != RE::row_of(J - 1) / C::ROWS) {
+            constexpr int gi = c_cur + C::S - 1;          // chunk refilled now, relative to this tile
             __syncwarp();
             if (lane == 0) {
-                fence_proxy_async_smem();          // prior generic reads of the stage
-                issue(g_cons + C::S - 1);          // refill the stage consumed last
+                fence_proxy_async_smem();                 // prior generic reads of the stage
+                issue<gi / C::NCH, gi % C::NCH>((cons + C::S - 1) % C::S);
             }
-            const int st = (int)(g_cons % C::S);
-            mbar_wait(bar0 + 8u * st, (uint32_t)((g_cons / C::S) & 1));
+            const uint32_t st = cons % C::S;
+            mbar_wait(bar0 + 8u * st, (cons / C::S) & 1u);
             cur = ring + (size_t)st * C::ROWS * TILE + lane;
-            ++g_cons;
+            ++cons;
         }
     }
     template <int J>
     __device__ __forceinline__ void end() {}
     __device__ __forceinline__ double w(int k) const { return cur[(k % C::ROWS) * TILE]; }
+    __device__ __forceinline__ void next_tile() {
+        tptr += tstride;
+        --tiles_left;
+    }
 };
 
 // Theorem 1 storage (global WP diagonal over W = C_{N,2p}): the weight of
@@ -105,15 +143,69 @@ struct GatherPol {
     __device__ __forceinline__ double w(int k) const { return __ldg(wg + baseW + offw[k]); }
 };
 
-// 3 CTAs (12 warps) per SM where u_T + y_T fit in <= 170 registers, else 2
-#ifndef DOGIP_MINB_LARGE
-#define DOGIP_MINB_LARGE 2   // CTAs/SM asked of ptxas when V_T > 20 (3D P4)
-#endif
-template <int D, int P, int F, int ST>
-constexpr int min_blocks() { return dogip_gen::RefElem<D, P, F, ST>::VT <= 20 ? 3 : DOGIP_MINB_LARGE; }
+// Per-tile gather context of one lane's element.
+struct ElemCtx {
+    int64_t base;          // DoF index of the cell origin
+    int v1, v2, v3;        // DoF-lattice offsets of vertices 1..d
+    uint64_t skip;         // bit l: local DoF l is not gathered / scattered (Dirichlet)
+    bool valid;            // lane holds a real element (ci < Nx)
+    int s, ci, cj, ck;
+};
+
+template <class RE, int D, bool DIR>
+__device__ __forceinline__ ElemCtx elem_ctx(const SlabGeo& geo, const ApplyTables& tab, int64_t t, int lane) {
+    const TileCoord tc = tile_coord(geo, t);
+    ElemCtx c;
+    c.s = tc.s; c.ci = tc.ci0 + lane; c.cj = tc.cj; c.ck = tc.ck;
+    c.valid = c.ci < geo.Nx;
+    c.base = (int64_t)geo.p * (c.ci + geo.sy * tc.cj + geo.sz * tc.ck);
+    c.v1 = tab.vstr[tc.s][0];
+    c.v2 = tab.vstr[tc.s][1];
+    c.v3 = D == 3 ? tab.vstr[tc.s][2] : 0;
+    c.skip = 0;
+    if constexpr (DIR) {   // boundary DoFs = DoFs on a cell face that lies on the domain boundary
+        const unsigned long long* fm = tab.fmask[tc.s];
+        uint64_t b = 0;
+        if (c.ci == 0) b |= fm[0];
+        if (c.ci == geo.Nx - 1) b |= fm[1];
+        if (D == 3) {
+            if (tc.cj == 0) b |= fm[2];
+            if (tc.cj == geo.Ny - 1) b |= fm[3];
+            if (tc.ck == 0 && geo.bnd_lo) b |= fm[4];
+            if (tc.ck == geo.Nz - 1 && geo.bnd_hi) b |= fm[5];
+        } else {
+            if (tc.cj == 0 && geo.bnd_lo) b |= fm[2];
+            if (tc.cj == geo.Ny - 1 && geo.bnd_hi) b |= fm[3];
+        }
+        c.skip = b;
+    }
+    return c;
+}
+
+template <class RE, int L>
+__device__ __forceinline__ int dof_off(const ElemCtx& c) {
+    return RE::ALPHA[L][0] * c.v1 + RE::ALPHA[L][1] * c.v2 + RE::ALPHA[L][2] * c.v3;
+}
+
+template <class RE, int L = 0>
+__device__ __forceinline__ void gather(const double* __restrict__ u, const ElemCtx& c, double* uT) {
+    if constexpr (L < RE::VT) {
+        const bool take = c.valid && !((c.skip >> L) & 1ull);
+        uT[L] = take ? ldg_f64(u + c.base + dof_off<RE, L>(c)) : 0.0;
+        gather<RE, L + 1>(u, c, uT);
+    }
+}
+
+template <class RE, int L = 0>
+__device__ __forceinline__ void scatter(double* __restrict__ y, const ElemCtx& c, const double* yT) {
+    if constexpr (L < RE::VT) {
+        if (!((c.skip >> L) & 1ull)) red_add_f64(y + c.base + dof_off<RE, L>(c), yT[L]);
+        scatter<RE, L + 1>(y, c, yT);
+    }
+}
 
 template <int D, int P, int F, int ST, bool DIR, bool GLOB>
-__global__ void __launch_bounds__(APPLY_THREADS, min_blocks<D, P, F, ST>())
+__global__ void __launch_bounds__(APPLY_THREADS, min_blocks<dogip_gen::RefElem<D, P, F, ST>>())
 apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
              const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end,
              double* __restrict__ dot_partials, const int* __restrict__ offw_g) {
@@ -122,22 +214,20 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     constexpr int NW = APPLY_THREADS / 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* rings = reinterpret_cast<double*>(smem_raw);
-    double* ubufs = rings + (size_t)NW * C::S * C::ROWS * TILE;          // [NW][VT][32]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ubufs + (size_t)NW * RE::VT * TILE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)NW * C::S * C::ROWS * TILE);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t gw = tile_begin + (int64_t)blockIdx.x * NW + warp;
+    const int64_t nw = (int64_t)gridDim.x * NW;
     WarpStream<RE> ws;
     ws.ring = rings + (size_t)warp * C::S * C::ROWS * TILE;
     ws.bar0 = smem_u32(bars + warp * C::S);
     ws.lane = lane;
-    ws.wbase = w;
-    ws.gw = tile_begin + (int64_t)blockIdx.x * NW + warp;
-    ws.nw = (int64_t)gridDim.x * NW;
-    ws.tile_end = tile_end;
-    ws.g_cons = 0;
+    ws.tptr = w + gw * C::TILE_DBL;
+    ws.tstride = nw * C::TILE_DBL;
+    ws.tiles_left = gw < tile_end ? (tile_end - gw + nw - 1) / nw : 0;
+    ws.cons = 0;
     ws.policy = policy_evict_first();
-    double* ubuf = ubufs + (size_t)warp * RE::VT * TILE;
-    const uint32_t ubuf_s = smem_u32(ubuf + lane);
     __shared__ int offw_s[GLOB ? MAX_NS * MAX_WT_GLOBAL : 1];
     if constexpr (GLOB) {
         for (int i = threadIdx.x; i < MAX_NS * RE::WT; i += blockDim.x)
@@ -146,82 +236,41 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     } else if (lane == 0) {
         for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
         fence_mbar_init();
-        for (int s = 0; s < C::S - 1; ++s) ws.issue(s);      // prologue of the weight stream
+        ws.prologue();                                   // prologue of the weight stream
     }
-    // u_T of a tile -> this lane's column of the warp's u buffer (cp.async, no registers)
-    auto prefetch_u = [&](int64_t t) {
-        const TileCoord tc = tile_coord(geo, t);
-        const int ci = tc.ci0 + lane;
-        if (ci < geo.Nx) {
-            const double* ub = u + (int64_t)geo.p * (ci + geo.sy * tc.cj + geo.sz * tc.ck);
-            const int* off = tab.off + tc.s * MAX_VT;
-#pragma unroll
-            for (int l = 0; l < RE::VT; ++l) cp_async8(ubuf_s + 8u * TILE * l, ub + off[l]);
-        }
-        cp_async_commit();
-    };
-    if (DOGIP_UPREFETCH && ws.gw < tile_end) prefetch_u(ws.gw);
     __syncwarp();
 
     double udot = 0.0;
-    for (int64_t tile = ws.gw; tile < tile_end; tile += ws.nw) {
-        const TileCoord tc = tile_coord(geo, tile);
-        const int ci = tc.ci0 + lane;
-        const bool valid = ci < geo.Nx;
-        const int64_t base = (int64_t)geo.p * (ci + geo.sy * tc.cj + geo.sz * tc.ck);
-        const int* off = tab.off + tc.s * MAX_VT;
-        const int* lof = tab.loff + tc.s * MAX_VT;
-        double uT[RE::VT], yT[RE::VT];
-        uint64_t bmask = 0;
-        if (DOGIP_UPREFETCH) {
-            cp_async_wait_all();
-            __syncwarp();
-        }
+    double uT[RE::VT];
+    ElemCtx cur{};
+    if (gw < tile_end) {
+        cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
+        gather<RE>(u, cur, uT);
+    }
+    for (int64_t tile = gw; tile < tile_end; tile += nw) {
+        double yT[RE::VT];
 #pragma unroll
-        for (int l = 0; l < RE::VT; ++l) {
-            bool take = valid;
-            if constexpr (DIR) {
-                const int lo = lof[l];
-                const int X = geo.p * ci + (lo & 0xff);
-                const int Y = geo.p * tc.cj + ((lo >> 8) & 0xff);
-                const int Z = geo.p * tc.ck + ((lo >> 16) & 0xff);
-                bool b = X == 0 || X == geo.pmax_x;
-                if (D == 3) {
-                    b = b || Y == 0 || Y == geo.pmax_y || (Z == 0 && geo.bnd_lo) || (Z == geo.pmax_z && geo.bnd_hi);
-                } else {
-                    b = b || (Y == 0 && geo.bnd_lo) || (Y == geo.pmax_y && geo.bnd_hi);
-                }
-                if (b) { bmask |= (1ull << l); take = false; }
-            }
-            if (DOGIP_UPREFETCH) {
-                const double v = ubuf[l * TILE + lane];
-                uT[l] = take ? v : 0.0;
-            } else {
-                uT[l] = take ? ldg_f64(u + base + off[l]) : 0.0;
-            }
-            yT[l] = 0.0;
-        }
-        if (DOGIP_UPREFETCH) {
-            __syncwarp();
-            if (tile + ws.nw < tile_end) prefetch_u(tile + ws.nw);  // overlaps this tile's compute
-        }
+        for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
         if constexpr (GLOB) {
-            GatherPol gp{w, offw_s + tc.s * MAX_WT_GLOBAL,
-                         (int64_t)(2 * geo.p) * (ci + geo.swy * tc.cj + geo.swz * tc.ck)};
+            GatherPol gp{w, offw_s + cur.s * MAX_WT_GLOBAL,
+                         (int64_t)(2 * geo.p) * (cur.ci + geo.swy * cur.cj + geo.swz * cur.ck)};
             RE::body(uT, yT, gp);
         } else {
             RE::body(uT, yT, ws);
+            ws.next_tile();
         }
-        if (valid) {
-#pragma unroll
-            for (int l = 0; l < RE::VT; ++l) {
-                if (DIR && ((bmask >> l) & 1ull)) continue;
-                red_add_f64(y + base + off[l], yT[l]);
-            }
-            // u^T A u = sum_T u_T^T (Bhat^T A_T Bhat u_T): the CG dot p.q, element by element
+        // u^T A u = sum_T u_T^T (Bhat^T A_T Bhat u_T): the CG dot p.q, element by element
+        // (padding lanes and Dirichlet DoFs have u_T = 0 and contribute nothing)
+        if (dot_partials) {
 #pragma unroll
             for (int l = 0; l < RE::VT; ++l) udot = fma(uT[l], yT[l], udot);
         }
+        const ElemCtx prev = cur;
+        if (tile + nw < tile_end) {            // next tile's gather overlaps this scatter
+            cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
+            gather<RE>(u, cur, uT);
+        }
+        if (prev.valid) scatter<RE>(y, prev, yT);
     }
     if (dot_partials) {     // deterministic: one partial per warp, fixed order reduction later
         for (int o = 16; o > 0; o >>= 1) udot += __shfl_xor_sync(0xffffffffu, udot, o);
@@ -234,8 +283,7 @@ cudaError_t launch_one(const ApplyArgs& a) {
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
-    const size_t smem = (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * RE::VT * TILE * 8 +
-                        (size_t)NW * C::S * 8;
+    const size_t smem = GLOB ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8;
     auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
     static int configured = 0;   // per instantiation
     static int occ = 1;

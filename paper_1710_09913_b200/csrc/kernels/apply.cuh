@@ -22,6 +22,11 @@ constexpr int APPLY_MAX_WARPS = 148 * 8 * 4;   // bound of the per-warp dot part
 struct ApplyTables {
     int off[MAX_NS * MAX_VT];
     int loff[MAX_NS * MAX_VT];
+    // apply kernel: DoF-lattice offset of vertex i = 1..d of simplex s (v_0 = cell origin),
+    // so off[s][l] = sum_i alpha_i(l) vstr[s][i-1] with compile-time alpha
+    int vstr[MAX_NS][3];
+    // DoFs of simplex s on the cell face "axis a at 0" (bit 2a) / "axis a at p" (2a+1)
+    unsigned long long fmask[MAX_NS][6];
 };
 
 constexpr int MAX_WT_GLOBAL = 165;   // W_T of P_8 in 3D (global WP storage, p <= 4)
