@@ -74,6 +74,9 @@ extern "C" {
                                 as a W-lattice vector ((2pN+1)^d doubles) holding A_ii / mult_i
                                 (mult_i = elements sharing W node i, each visits it once) and
                                 gathered per element; multi-rank needs the NCCL communicator */
+#define DOGIP_STORE_PAIR   3 /* WP only: the values of DOGIP_STORE_FULL in the paired-lane layout
+                                (two lanes per element, node pairs (j, sigma j) in adjacent rows of
+                                16-element half-tiles); same bytes, fewer registers per lane */
 
 /* ---- status codes ------------------------------------------------------- */
 #define DOGIP_OK                     0

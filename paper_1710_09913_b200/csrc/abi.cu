@@ -305,8 +305,11 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     if (!m || !out) return fail(DOGIP_E_INVALID_ARG, "null argument");
     *out = nullptr;
     if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
-    if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO && storage != DOGIP_STORE_GLOBAL)
+    if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO && storage != DOGIP_STORE_GLOBAL &&
+        storage != DOGIP_STORE_PAIR)
         return fail(DOGIP_E_INVALID_ARG, "unknown storage");
+    if (storage == DOGIP_STORE_PAIR && form != DOGIP_WP)
+        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_PAIR applies to the weighted projection only");
     if (storage == DOGIP_STORE_ISO && form != DOGIP_EL)
         return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_ISO applies to the elliptic form only");
     if (storage == DOGIP_STORE_GLOBAL && form != DOGIP_WP)
@@ -355,7 +358,9 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
 
     DevBufs tmp;
     WeightsArgs a{};
-    a.d = d; a.p = p; a.form = form; a.store = storage == DOGIP_STORE_GLOBAL ? 0 : storage;
+    a.d = d; a.p = p; a.form = form;
+    a.store = (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_PAIR) ? 0 : storage;
+    a.pair = storage == DOGIP_STORE_PAIR;
     a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
     a.NG = op->ref.NG; a.tile_rows = op->ref.tile_rows;
     a.kind = coeff->kind;
@@ -381,6 +386,12 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         cudaMemcpy(dcell, coeff->per_cell, sizeof(double) * ncell, cudaMemcpyHostToDevice);
     }
     a.params = dparams; a.qp = dqp; a.qw = dqw; a.phiW = dphi; a.sW = dsW; a.per_cell = dcell; a.bad_flag = dbad;
+    if (a.pair) {
+        int* drp = nullptr;
+        if (tmp.alloc(&drp, WT)) return cleanup_fail(DOGIP_E_OOM, "row permutation");
+        cudaMemcpy(drp, op->ref.rowperm, sizeof(int) * WT, cudaMemcpyHostToDevice);
+        a.rowperm = drp;
+    }
     const bool direct = coeff->kind == DOGIP_COEF_CONST || coeff->kind == DOGIP_COEF_PER_CELL ||
                         coeff->kind == DOGIP_COEF_CONST_TENSOR;
     int64_t batch = (int64_t)(256ll << 20) / (8ll * ncomp * std::max(nq, WT));
@@ -867,7 +878,11 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
                 for (int j = 0; j < WT; ++j) host[e * WT + j] = w[bw + offw[(size_t)tc.s * WT + j]];
                 continue;
             }
-            auto at = [&](int row) { return w[((size_t)t * TR + row) * TILE + lane]; };
+            auto at = [&](int row) {
+                if (op->store == DOGIP_STORE_PAIR)   // half-tiles of 16, node rows permuted
+                    return w[((size_t)(2 * t + lane / 16) * TR + op->ref.rowperm[row]) * 16 + lane % 16];
+                return w[((size_t)t * TR + row) * TILE + lane];
+            };
             for (int j = 0; j < WT; ++j)
                 for (int c = 0; c < NC; ++c)
                     host[(e * WT + j) * NC + c] =

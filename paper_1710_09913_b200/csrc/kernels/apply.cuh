@@ -32,7 +32,8 @@ struct ApplyTables {
 constexpr int MAX_WT_GLOBAL = 165;   // W_T of P_8 in 3D (global WP storage, p <= 4)
 
 struct ApplyArgs {
-    int d, p, form, store;      // store: 0 full A_T blocks, 1 isotropic a_j + G_T (EL), 2 global WP
+    int d, p, form, store;      // store: 0 full A_T blocks, 1 isotropic a_j + G_T (EL), 2 global WP,
+                                // 3 full WP in the paired-lane layout
     bool dirichlet;
     const double* u;
     double* y;
@@ -52,7 +53,9 @@ cudaError_t launch_apply(const ApplyArgs& a);
 // Constants of the generated reference element (generated/bhat_gen.cuh).
 struct RefInfo {
     int VT, WT, NC, NG, NS, tile_rows, flops, nnz, nnz_pm1;
+    int pair;                        // paired-lane WP layout (STORE 3): half-tiles of 16, rows permuted
     int loff[MAX_NS][MAX_VT][3];
+    int rowperm[MAX_WT_GLOBAL];      // storage row of canonical node j (identity unless pair)
 };
 bool ref_info(int d, int p, int form, int store, RefInfo& r);
 
@@ -75,6 +78,8 @@ struct WeightsArgs {
     double* scratch_a;                     // [nb * ncomp][WT]
     int64_t batch;                         // elements per batch (multiple of 32)
     int* bad_flag;                         // device int: 1 degenerate element, 2 bad coefficient
+    int pair;                              // paired-lane WP layout (STORE 3)
+    const int* rowperm;                    // device (WT,): storage row of node j (pair layout)
     cudaStream_t stream;
 };
 cudaError_t launch_weights(const WeightsArgs& a);

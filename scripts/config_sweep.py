@@ -61,6 +61,8 @@ def main():
             variants.append((1, 1))
         if args.iso and 0 in forms and c.p <= 4:
             variants.append((0, 2))
+        if args.iso and 0 in forms:
+            variants.append((0, 3))
         for form, storage in variants:
             op = Operator(mesh, form, coef, storage=storage)
             oi = op.info
@@ -69,7 +71,7 @@ def main():
             dirichlet = form == 1
             n = args.iters if c.ndof > 1e6 else 200
             t_apply = time_apply(op, u, y, n, dirichlet)
-            nw = oi["W_T"] * oi["n_c"] if storage == 0 else oi["W_T"] + oi["n_c"]
+            nw = oi["W_T"] + oi["n_c"] if storage == 1 else oi["W_T"] * oi["n_c"]
             alg = 8 * nw * c.n_elem + 16 * c.ndof
             if storage == 2:                      # global W vector read once (Theorem 1)
                 alg = oi["weight_bytes"] + 16 * c.ndof
@@ -77,7 +79,7 @@ def main():
             x = torch.zeros_like(b)
             op.cg(b, x, maxit=-3, dirichlet=dirichlet)
             r = op.cg(b, x, maxit=-n, dirichlet=dirichlet, resume=True)
-            row = {"config": name, "form": ["WP", "EL", "EL-iso", "WP-glob"][form if storage == 0 else storage + 1],
+            row = {"config": name, "form": ["WP", "EL", "EL-iso", "WP-glob", "WP-pair"][form if storage == 0 else storage + 1],
                    "d": c.d, "N": c.N, "p": c.p, "flops_per_elem": oi["flops_per_elem"],
                    "fp64_TFs": oi["flops_per_elem"] * c.n_elem / t_apply / 1e12,
                    "n_elem": c.n_elem, "ndof": c.ndof, "W_T": oi["W_T"], "n_c": oi["n_c"],
