@@ -307,7 +307,9 @@ def run_product(args, cfg) -> None:
                             "fp64_frac_of_measured_dfma": flops_apply / t_apply / 1e12 / FP64_PEAK_TFLOPS},
                "e2e": {"value": info["ndof_global"] / t_e2e.item() / 1e9, "unit": UNIT,
                        "h2d_bytes_per_step": int(tot_vec.item()), "d2h_bytes_per_step": int(tot_vec.item()),
-                       "api": "dogip_apply_host (pinned host u -> device, apply, device -> host y)"},
+                       "api": "dogip_apply_host (pinned host u -> device, apply, device -> host y; "
+                              "pipelined over 16 chunks of cube layers on copy-in / compute / copy-out "
+                              "streams when single-rank)"},
                "gpu_launches": int(launches),
                "clocks": clocks}
         if world == 1 and not args.no_cpu_baseline:

@@ -217,9 +217,14 @@ int dogip_op_info(dogip_op op, dogip_op_info_t* out);
 int dogip_apply(dogip_op op, const double* u, double* y, unsigned flags, void* stream);
 
 /*
- * dogip_apply_host -- the same apply with HOST buffers: copies u (ndof_local
- * doubles) host->device, applies, copies y device->host into a library-owned
- * device scratch, synchronises `stream`.  Pinned host memory is fastest.
+ * dogip_apply_host -- the same apply with HOST buffers u_host, y_host (ndof_local
+ * doubles each, caller-owned; pinned memory is needed for the copies to overlap).
+ * Single rank: pipelined over up to 16 chunks of cube layers along the slab axis --
+ * copy-in of the next chunk's u planes, the apply kernel of this chunk's elements and
+ * copy-out of the y planes it completed run concurrently on three streams (library-
+ * owned device scratch and copy streams, ordered after prior work on `stream`).
+ * Several ranks with exchange: copy in, dogip_apply, copy out.  Synchronises.
+ * Errors: E_INVALID_ARG (null buffer, unknown flags), E_OOM, E_CUDA, E_NCCL.
  */
 int dogip_apply_host(dogip_op op, const double* u_host, double* y_host, unsigned flags,
                      void* stream);

@@ -77,6 +77,9 @@ struct dogip_op_s {
     double* dotp = nullptr;    // per-warp partials of p^T A p (3 launches x APPLY_MAX_WARPS)
     double* bpart = nullptr;   // boundary-row partials of the Dirichlet fix-up (RED_BLOCKS)
     float weights_ms = 0.f;
+    // pipelined host-buffer apply: copy-in / copy-out streams, one event pair per chunk
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    std::vector<cudaEvent_t> ev_in, ev_done;
 };
 
 static int64_t ipow(int64_t b, int e) {
@@ -486,6 +489,10 @@ extern "C" void dogip_op_destroy(dogip_op op) {
         cudaFree(x);
     cudaFree(op->d_offw);
     if (op->h_scal) cudaFreeHost(op->h_scal);
+    for (cudaEvent_t e : op->ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : op->ev_done) cudaEventDestroy(e);
+    if (op->s_h2d) cudaStreamDestroy(op->s_h2d);
+    if (op->s_d2h) cudaStreamDestroy(op->s_d2h);
     delete op;
 }
 
@@ -590,14 +597,82 @@ extern "C" int dogip_apply(dogip_op op, const double* u, double* y, unsigned fla
     return apply_impl(op, u, y, flags, (cudaStream_t)stream);
 }
 
+// Host-buffer apply, pipelined over chunks of cube layers along the slab axis (single
+// rank): the copy-in of chunk c+1's u planes, the apply kernel of chunk c's elements
+// and the copy-out of the y planes chunk c completed run on three streams.  Tiles are
+// ordered with the slab axis slowest, so chunk c = layers [a, b) = tiles [a tpl, b tpl)
+// reads DoF planes [p a, p b] and completes planes [p a, p b) (the last chunk also p b).
+// Dirichlet rows (y_i = u_i) are written per completed plane range; the DIRICHLET apply
+// kernel never scatters into boundary DoFs, so the order against later chunks is free.
+static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_host, unsigned flags,
+                                cudaStream_t st) {
+    dogip_mesh_s* m = op->m;
+    const SlabGeo& g = m->geo;
+    const int64_t layers = g.d == 3 ? g.Nz : g.Ny;
+    const int64_t tpl = g.ntiles / layers;
+    const int64_t plane = g.d == 3 ? g.sz : g.sy;
+    const int p = m->p;
+    const int K = (int)std::min<int64_t>(layers, 16);
+    const bool dir = (flags & DOGIP_DIRICHLET_ZERO) != 0;
+    if (!op->s_h2d) {
+        CK(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&op->s_d2h, cudaStreamNonBlocking));
+    }
+    while ((int)op->ev_in.size() < K + 1) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+        op->ev_in.push_back(a);
+        op->ev_done.push_back(b);
+    }
+    // the caller's stream orders us after its prior work; y starts from zero (atomics)
+    CK(cudaEventRecord(op->ev_in[K], st));
+    CK(cudaStreamWaitEvent(op->s_h2d, op->ev_in[K], 0));
+    CK(cudaMemsetAsync(op->hy, 0, sizeof(double) * g.ndof, st));
+    int64_t in_end = 0, out_end = 0;   // DoF planes copied in / out so far
+    for (int c = 0; c < K; ++c) {
+        const int64_t a = layers * c / K, b = layers * (c + 1) / K;
+        const int64_t need = p * b + 1;                         // planes [0, p b] resident
+        CK(cudaMemcpyAsync(op->hu + in_end * plane, u_host + in_end * plane,
+                           sizeof(double) * (need - in_end) * plane, cudaMemcpyHostToDevice, op->s_h2d));
+        in_end = need;
+        CK(cudaEventRecord(op->ev_in[c], op->s_h2d));
+        CK(cudaStreamWaitEvent(st, op->ev_in[c], 0));
+        ApplyArgs aa{};
+        aa.d = m->d; aa.p = p; aa.form = op->form; aa.store = op->store;
+        aa.offw = op->d_offw;
+        aa.dirichlet = dir;
+        aa.u = op->hu; aa.y = op->hy; aa.w = op->d_w; aa.geo = g; aa.tab = &m->tab;
+        aa.num_sms = m->num_sms;
+        aa.stream = st;
+        aa.tile_begin = a * tpl;
+        aa.tile_end = b * tpl;
+        CK(launch_apply(aa));
+        const int64_t done = c == K - 1 ? p * b + 1 : p * b;    // planes [out_end, done) are final
+        if (dir) CK(launch_dirichlet_planes(g, op->hu, op->hy, out_end, done, st));
+        CK(cudaEventRecord(op->ev_done[c], st));
+        CK(cudaStreamWaitEvent(op->s_d2h, op->ev_done[c], 0));
+        CK(cudaMemcpyAsync(y_host + out_end * plane, op->hy + out_end * plane,
+                           sizeof(double) * (done - out_end) * plane, cudaMemcpyDeviceToHost, op->s_d2h));
+        out_end = done;
+    }
+    CK(cudaStreamSynchronize(op->s_d2h));
+    CK(cudaStreamSynchronize(st));
+    return DOGIP_OK;
+}
+
 extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_host, unsigned flags, void* stream) {
     if (!op || !u_host || !y_host) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = op->m->geo.ndof;
+    CK(cudaSetDevice(op->m->device));
     if (!op->hu) {
         CK(cudaMalloc(&op->hu, sizeof(double) * n));
         CK(cudaMalloc(&op->hy, sizeof(double) * n));
     }
+    const bool xchg = op->m->nranks > 1 && op->m->comm && !(flags & DOGIP_NO_EXCHANGE);
+    if (!xchg) return apply_host_pipelined(op, u_host, y_host, flags, st);
     CK(cudaMemcpyAsync(op->hu, u_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     RET(dogip_apply(op, op->hu, op->hy, flags, stream));
     CK(cudaMemcpyAsync(y_host, op->hy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));

@@ -92,6 +92,9 @@ cudaError_t launch_globalize(const SlabGeo& g, int WT, const double* wel, const 
 // ----------------------------------------------------------- vectors / CG
 cudaError_t launch_dirichlet_fixup(const SlabGeo& g, const double* u, double* y, cudaStream_t st);
 cudaError_t launch_zero_boundary(const SlabGeo& g, double* y, cudaStream_t st);
+// y_i = u_i on the boundary DoFs of slab-axis DoF planes [P0, P1)
+cudaError_t launch_dirichlet_planes(const SlabGeo& g, const double* u, double* y, int64_t P0, int64_t P1,
+                                    cudaStream_t st);
 cudaError_t launch_load_vector(const SlabGeo& g, int p, const double* verts, const double* sV,
                                int VT, const ApplyTables* tab, double f, double* b, cudaStream_t st);
 

@@ -365,6 +365,33 @@ cudaError_t launch_add_planes(double* y, const double* lo, const double* hi, int
     return cudaGetLastError();
 }
 
+// Dirichlet rows y_i = u_i restricted to slab-axis DoF planes [P0, P1) (pipelined host apply)
+__global__ void __launch_bounds__(RED_THREADS) boundary_planes_kernel(SlabGeo g, const double* __restrict__ u,
+                                                                      double* __restrict__ y, int64_t P0, int64_t P1) {
+    const int64_t plane = g.d == 3 ? g.sz : g.sy;
+    const int64_t n = (P1 - P0) * plane;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t idx = P0 * plane + t;
+        const int64_t P = idx / plane, r = idx - P * plane;
+        const int64_t X = r % g.sy;
+        bool b = X == 0 || X == g.pmax_x || (P == 0 && g.bnd_lo) || (P == (g.d == 3 ? g.pmax_z : g.pmax_y) && g.bnd_hi);
+        if (g.d == 3) {
+            const int64_t Y = r / g.sy;
+            b = b || Y == 0 || Y == g.pmax_y;
+        }
+        if (b) y[idx] = u[idx];
+    }
+}
+
+cudaError_t launch_dirichlet_planes(const SlabGeo& g, const double* u, double* y, int64_t P0, int64_t P1,
+                                    cudaStream_t st) {
+    const int64_t plane = g.d == 3 ? g.sz : g.sy;
+    if (P1 <= P0) return cudaSuccess;
+    boundary_planes_kernel<<<grid_for((P1 - P0) * plane, RED_THREADS), RED_THREADS, 0, st>>>(g, u, y, P0, P1);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_dirichlet_fixup(const SlabGeo& g, const double* u, double* y, cudaStream_t st) {
     boundary_set_kernel<<<grid_for(boundary_count(g), RED_THREADS), RED_THREADS, 0, st>>>(g, u, y, 0, 0, nullptr);
     count_launches(1);

@@ -240,16 +240,30 @@ def test_slab_partials_sum_to_global(d, N, p, form, nr):
     assert relerr(acc, y_glob) <= 1e-14
 
 
-def test_apply_host_matches_device():
+HOST_CASES = [("C4", 9, 1, 0, False), ("C4", 9, 1, 0, True), ("C4", 37, 1, 0, True), ("C2p2", 40, 1, 0, True),
+              ("C5", 5, 0, 0, False), ("C5", 19, 0, 3, False), ("C5", 6, 0, 2, False), ("C1", 16, 0, 0, False),
+              ("C3", 1, 1, 0, True)]
+
+
+@pytest.mark.parametrize("name,N,form,storage,dirichlet", HOST_CASES)
+def test_apply_host_matches_device(name, N, form, storage, dirichlet):
+    """dogip_apply_host (pipelined over chunks of cube layers: copy-in / apply / copy-out
+    on three streams, per-plane Dirichlet rows) equals the device apply; N = 37 gives
+    16 uneven chunks, N = 1 a single layer."""
     torch = _torch()
     from paper_1710_09913_b200.api import Mesh, Operator
-    c = get_config("C4").with_size(9)
-    m = Mesh(3, c.N, c.p)
-    op = Operator(m, 1, c.coefficient())
+    c = get_config(name).with_size(N)
+    m = Mesh(c.d, c.N, c.p, c.vertices())
+    op = Operator(m, form, c.coefficient(), storage=storage)
     u = c.u()
-    yd = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
-    yh = op.apply_host(u)
-    assert relerr(yh, yd) <= 1e-14
+    yd = op.apply(torch.from_numpy(u).cuda(), dirichlet=dirichlet).cpu().numpy()
+    uh = torch.from_numpy(u).pin_memory()
+    yh = torch.empty_like(uh).pin_memory()
+    for _ in range(2):       # twice: reuse of the library's streams / events / scratch
+        yh.fill_(np.nan)
+        op.apply_host_ptr(uh.data_ptr(), yh.data_ptr(), dirichlet=dirichlet)
+        assert relerr(yh.numpy(), yd) <= 1e-14
+    assert relerr(op.apply_host(u, dirichlet=dirichlet), yd) <= 1e-14   # pageable buffers
 
 
 def test_negative_control_other_rule_fails():
