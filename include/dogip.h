@@ -77,6 +77,12 @@ extern "C" {
 #define DOGIP_STORE_PAIR   3 /* WP only: the values of DOGIP_STORE_FULL in the paired-lane layout
                                 (two lanes per element, node pairs (j, sigma j) in adjacent rows of
                                 16-element half-tiles); same bytes, fewer registers per lane */
+#define DOGIP_STORE_QP     4 /* no DoGIP weights: the quadrature-point matrix-free comparator
+                                ("alternative approaches") -- geometry, coefficient and the
+                                basis contractions at the n_q points of the contract rule (L10) are
+                                evaluated on the fly every apply; same operator A up to rounding.
+                                Stores only the basis tables and the coefficient data; does not
+                                validate coefficient positivity or element orientation */
 
 /* ---- status codes ------------------------------------------------------- */
 #define DOGIP_OK                     0

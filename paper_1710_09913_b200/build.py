@@ -22,7 +22,7 @@ LIB = os.path.join(PKG, "libdogip.so")
 GEN_OUT = os.path.join(CSRC, "generated", "bhat_gen.cuh")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CU_SOURCES = ["abi.cu", "kernels/apply.cu", "kernels/weights.cu", "kernels/vectors.cu"]
+CU_SOURCES = ["abi.cu", "kernels/apply.cu", "kernels/weights.cu", "kernels/vectors.cu", "kernels/qp.cu"]
 
 
 def _headers():

@@ -77,6 +77,10 @@ struct dogip_op_s {
     double* dotp = nullptr;    // per-warp partials of p^T A p (3 launches x APPLY_MAX_WARPS)
     double* bpart = nullptr;   // boundary-row partials of the Dirichlet fix-up (RED_BLOCKS)
     float weights_ms = 0.f;
+    // quadrature-point comparator (DOGIP_STORE_QP): tables and coefficient data
+    double *q_pts = nullptr, *q_wts = nullptr, *q_phi = nullptr, *q_dphi = nullptr, *q_params = nullptr,
+           *q_cell = nullptr;
+    int q_kind = 0, q_ncomp = 1, q_nq = 0;
     // pipelined host-buffer apply: copy-in / copy-out streams, one event pair per chunk
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_done;
@@ -309,7 +313,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     *out = nullptr;
     if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
     if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO && storage != DOGIP_STORE_GLOBAL &&
-        storage != DOGIP_STORE_PAIR)
+        storage != DOGIP_STORE_PAIR && storage != DOGIP_STORE_QP)
         return fail(DOGIP_E_INVALID_ARG, "unknown storage");
     if (storage == DOGIP_STORE_PAIR && form != DOGIP_WP)
         return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_PAIR applies to the weighted projection only");
@@ -331,7 +335,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     op->m = m;
     op->form = form;
     op->store = storage;
-    ref_info(d, p, form, storage == DOGIP_STORE_GLOBAL ? 0 : storage, op->ref);
+    ref_info(d, p, form, (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_QP) ? 0 : storage, op->ref);
     const int WT = op->ref.WT, NC = op->ref.NC, VT = op->ref.VT;
     const int n1d = quad_n1d > 0 ? quad_n1d : p + 3;
     std::vector<double> pts, wts;
@@ -352,8 +356,34 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         for (int q = 0; q < nq; ++q) s += (long double)wts[q] * phiV[(size_t)q * VT + l];
         sV[l] = (double)s;
     }
-    op->w_doubles = m->geo.ntiles * (int64_t)op->ref.tile_rows * TILE;
+    op->w_doubles = storage == DOGIP_STORE_QP ? 0 : m->geo.ntiles * (int64_t)op->ref.tile_rows * TILE;
     auto cleanup_fail = [&](int code, const std::string& msg) { dogip_op_destroy(op); return fail(code, msg); };
+    if (storage == DOGIP_STORE_QP) {
+        // matrix-free comparator: basis values / reference gradients at the n_q points of
+        // the same rule, coefficient parameters and per-cell values; nothing per element
+        std::vector<double> dphiV((size_t)nq * d * VT);
+        eval_grad_ld(d, p, pts.data(), nq, dphiV.data());
+        auto up = [&](double** dst, const double* src, size_t n) {
+            if (cudaMalloc(dst, sizeof(double) * std::max<size_t>(n, 1)) != cudaSuccess) return false;
+            if (n) cudaMemcpy(*dst, src, sizeof(double) * n, cudaMemcpyHostToDevice);
+            return true;
+        };
+        if (!up(&op->d_sV, sV.data(), VT) || !up(&op->q_pts, pts.data(), pts.size()) ||
+            !up(&op->q_wts, wts.data(), wts.size()) || !up(&op->q_phi, phiV.data(), phiV.size()) ||
+            !up(&op->q_dphi, dphiV.data(), dphiV.size()) ||
+            !up(&op->q_params, coeff->params, (size_t)coeff->nparams))
+            return cleanup_fail(DOGIP_E_OOM, "quadrature tables");
+        if (coeff->kind == DOGIP_COEF_PER_CELL && !up(&op->q_cell, coeff->per_cell, (size_t)ipow(m->N, d)))
+            return cleanup_fail(DOGIP_E_OOM, "per-cell coefficient");
+        op->q_kind = coeff->kind;
+        op->q_ncomp = ncomp;
+        op->q_nq = nq;
+        // FP64 flops per element per apply: interpolation + projection at every point
+        // (coefficient evaluation and congruence not counted)
+        op->ref.flops = form == DOGIP_WP ? nq * (4 * VT + 3) : nq * (4 * d * VT + 2 * d * d + d);
+        *out = op;
+        return DOGIP_OK;
+    }
     if (cudaMalloc(&op->d_w, sizeof(double) * op->w_doubles) != cudaSuccess)
         return cleanup_fail(DOGIP_E_OOM, "weights allocation (" + std::to_string(op->w_doubles * 8) + " bytes)");
     if (cudaMalloc(&op->d_sV, sizeof(double) * VT) != cudaSuccess) return cleanup_fail(DOGIP_E_OOM, "sV");
@@ -472,7 +502,8 @@ extern "C" int dogip_op_info(dogip_op op, dogip_op_info_t* o) {
     o->V_T = op->ref.VT; o->W_T = op->ref.WT;
     o->n_c = op->form == DOGIP_WP ? 1 : op->m->d * (op->m->d + 1) / 2;
     o->storage = op->store;
-    o->stream_doubles_per_elem = op->store == DOGIP_STORE_GLOBAL ? 0 : op->ref.tile_rows;
+    o->stream_doubles_per_elem =
+        (op->store == DOGIP_STORE_GLOBAL || op->store == DOGIP_STORE_QP) ? 0 : op->ref.tile_rows;
     o->flops_per_elem = op->ref.flops;
     o->quad_n1d = op->nq;
     o->n_tiles = op->m->geo.ntiles;
@@ -488,6 +519,7 @@ extern "C" void dogip_op_destroy(dogip_op op) {
                       op->bpart})
         cudaFree(x);
     cudaFree(op->d_offw);
+    for (double* x : {op->q_pts, op->q_wts, op->q_phi, op->q_dphi, op->q_params, op->q_cell}) cudaFree(x);
     if (op->h_scal) cudaFreeHost(op->h_scal);
     for (cudaEvent_t e : op->ev_in) cudaEventDestroy(e);
     for (cudaEvent_t e : op->ev_done) cudaEventDestroy(e);
@@ -525,6 +557,20 @@ static int finish_exchange(dogip_mesh_s* m, double* y, cudaStream_t st) {
     return DOGIP_OK;
 }
 
+// the comparator's launch arguments for the same tile range / flags as an apply
+static QpArgs qp_args(dogip_op op, const ApplyArgs& a) {
+    QpArgs q{};
+    q.d = a.d; q.p = a.p; q.form = a.form; q.dirichlet = a.dirichlet;
+    q.u = a.u; q.y = a.y; q.geo = a.geo; q.tab = a.tab;
+    q.nq = op->q_nq; q.qp = op->q_pts; q.qw = op->q_wts; q.phi = op->q_phi; q.dphi = op->q_dphi;
+    q.kind = op->q_kind; q.ncomp = op->q_ncomp; q.params = op->q_params; q.per_cell = op->q_cell;
+    q.verts = op->m->d_verts;
+    q.tile_begin = a.tile_begin; q.tile_end = a.tile_end;
+    q.num_sms = a.num_sms; q.stream = a.stream;
+    q.dot_partials = a.dot_partials; q.dot_nslots = a.dot_nslots;
+    return q;
+}
+
 // y = A u (+ exchange); with dot != null also *dot = u^T y over this rank's elements
 // (+ boundary rows owned by this rank), fused into the apply kernel (CG's p.q).
 static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, cudaStream_t st,
@@ -551,6 +597,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
         a.dot_partials = dot ? op->dotp + (size_t)nl * APPLY_MAX_WARPS : nullptr;
         a.dot_nslots = &nslots[nl];
         ++nl;
+        if (op->store == DOGIP_STORE_QP) return launch_qp_apply(qp_args(op, a));
         return launch_apply(a);
     };
     const bool xchg = m->nranks > 1 && m->comm && !(flags & DOGIP_NO_EXCHANGE);
@@ -647,7 +694,7 @@ static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_hos
         aa.stream = st;
         aa.tile_begin = a * tpl;
         aa.tile_end = b * tpl;
-        CK(launch_apply(aa));
+        CK(op->store == DOGIP_STORE_QP ? launch_qp_apply(qp_args(op, aa)) : launch_apply(aa));
         const int64_t done = c == K - 1 ? p * b + 1 : p * b;    // planes [out_end, done) are final
         if (dir) CK(launch_dirichlet_planes(g, op->hu, op->hy, out_end, done, st));
         CK(cudaEventRecord(op->ev_done[c], st));
@@ -929,6 +976,7 @@ static int64_t canonical_elem(const SlabGeo& g, int64_t tile, int lane) {
 
 extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
     if (!op || !host) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (op->store == DOGIP_STORE_QP) return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_QP stores no weights");
     dogip_mesh_info_t info;
     dogip_mesh_info(op->m, &info);
     const int d = op->m->d, WT = op->ref.WT, TR = op->ref.tile_rows;

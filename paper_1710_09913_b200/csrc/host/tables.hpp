@@ -185,6 +185,39 @@ inline void eval_basis_ld(int d, int k, const double* pts, int npts, double* out
     }
 }
 
+// Reference gradients d phi_c / d xhat_r = d/d lambda_r - d/d lambda_0 of P_k at points
+// (long double product rule), out[(q * d + r) * dim + c].
+inline void eval_grad_ld(int d, int k, const double* pts, int npts, double* out) {
+    auto A = multi_indices(d, k);
+    const int nb = (int)A.size();
+    for (int q = 0; q < npts; ++q) {
+        long double lam[4];
+        long double s = 0;
+        for (int r = 0; r < d; ++r) { lam[r + 1] = pts[q * d + r]; s += lam[r + 1]; }
+        lam[0] = 1.0L - s;
+        for (int c = 0; c < nb; ++c) {
+            long double f[4], df[4];   // factor of coordinate i and its derivative in lambda_i
+            for (int i = 0; i <= d; ++i) {
+                long double v = 1.0L, dv = 0.0L;
+                for (int m = 0; m < A[c][i]; ++m) {
+                    const long double t = ((long double)k * lam[i] - m) / (m + 1);
+                    dv = dv * t + v * (long double)k / (m + 1);
+                    v *= t;
+                }
+                f[i] = v;
+                df[i] = dv;
+            }
+            auto dlam = [&](int i) {
+                long double v = df[i];
+                for (int j = 0; j <= d; ++j)
+                    if (j != i) v *= f[j];
+                return v;
+            };
+            for (int r = 0; r < d; ++r) out[((size_t)q * d + r) * nb + c] = (double)(dlam(r + 1) - dlam(0));
+        }
+    }
+}
+
 // Simplex vertex offsets ({0,1}^d) of the d! simplices of one cell (reading L3).
 inline std::vector<std::array<std::array<int, 3>, 4>> cell_simplices(int d) {
     std::vector<std::array<std::array<int, 3>, 4>> out;

@@ -89,6 +89,33 @@ cudaError_t launch_divide(double* a, const double* b, int64_t n, cudaStream_t st
 cudaError_t launch_globalize(const SlabGeo& g, int WT, const double* wel, const int* offw, double* wg,
                              cudaStream_t st);
 
+// ----------------------------------------------------------- quadrature-point comparator
+// Matrix-free A u over the integration points, no stored operator.
+struct QpArgs {
+    int d, p, form;
+    bool dirichlet;
+    const double* u;
+    double* y;
+    SlabGeo geo;
+    const ApplyTables* tab;
+    int nq;
+    const double* qp;       // device (nq, d) reference points
+    const double* qw;       // device (nq,) weights
+    const double* phi;      // device (nq, V_T) basis values (WP)
+    const double* dphi;     // device (nq, d, V_T) reference gradients (EL)
+    int nq_smem;            // points whose table rows are staged in shared memory (set by the launcher)
+    int kind, ncomp;        // DOGIP_COEF_*, coefficient components
+    const double* params;   // device coefficient parameters
+    const double* per_cell; // device per-cell values or null
+    const double* verts;    // device vertices or null (lattice)
+    int64_t tile_begin, tile_end;
+    int num_sms;
+    cudaStream_t stream;
+    double* dot_partials;
+    int* dot_nslots;
+};
+cudaError_t launch_qp_apply(const QpArgs& a);
+
 // ----------------------------------------------------------- vectors / CG
 cudaError_t launch_dirichlet_fixup(const SlabGeo& g, const double* u, double* y, cudaStream_t st);
 cudaError_t launch_zero_boundary(const SlabGeo& g, double* y, cudaStream_t st);

@@ -13,161 +13,10 @@
 #include "../../../include/dogip.h"
 #include "apply.cuh"
 #include "common.cuh"
+#include "geometry.cuh"
 
 namespace dogip {
 namespace {
-
-struct Geo {
-    double R[3][3], Rinv[3][3], S[3], det;
-    int64_t cell;     // global cell index
-    bool valid;
-};
-
-// Simplex vertex offsets of one cell (reading L3): 2D right split, 3D Kuhn.
-__device__ __forceinline__ void simplex_offset(int d, int s, int v, int o[3]) {
-    o[0] = o[1] = o[2] = 0;
-    if (v == 0) return;
-    if (d == 2) {
-        if (s == 0) { o[0] = 1; o[1] = (v == 2); }
-        else { o[1] = 1; o[0] = (v == 1); }
-        return;
-    }
-    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-    for (int i = 0; i < v; ++i) o[perms[s][i]] += 1;
-}
-
-__device__ Geo element_geo(const SlabGeo& g, const double* verts, int64_t eK, int* bad) {
-    Geo G;
-    const int64_t tile = eK / TILE;
-    const int lane = (int)(eK % TILE);
-    const TileCoord tc = tile_coord(g, tile);
-    const int ci = tc.ci0 + lane;
-    G.valid = ci < g.Nx;
-    const int d = g.d;
-    int64_t c[3] = {ci, tc.cj, tc.ck};
-    if (d == 2) c[1] += g.zoff; else c[2] += g.zoff;
-    if (!G.valid) c[0] = 0;
-    G.cell = d == 2 ? c[0] + (int64_t)g.N * c[1] : c[0] + (int64_t)g.N * (c[1] + (int64_t)g.N * c[2]);
-    const int64_t M = g.N + 1;
-    double X[4][3];
-    int lat[4][3];
-    for (int v = 0; v <= d; ++v) {
-        int o[3];
-        simplex_offset(d, tc.s, v, o);
-        int64_t vid = 0, mul = 1;
-        for (int a = 0; a < d; ++a) {
-            lat[v][a] = o[a];
-            vid += (c[a] + o[a]) * mul;
-            mul *= M;
-        }
-        for (int a = 0; a < d; ++a)
-            X[v][a] = verts ? verts[vid * d + a] : (double)(c[a] + o[a]) / (double)g.N;
-    }
-    for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) G.R[a][b] = (a == b) ? 1.0 : 0.0;
-    for (int a = 0; a < d; ++a) {
-        G.S[a] = X[0][a];
-        for (int b = 0; b < d; ++b) G.R[a][b] = X[b + 1][a] - X[0][a];   // columns v_b - v_0
-    }
-    int Rl[3][3];
-    for (int a = 0; a < d; ++a)
-        for (int b = 0; b < d; ++b) Rl[a][b] = lat[b + 1][a] - lat[0][a];
-    int detl;
-    if (d == 2) {
-        G.det = G.R[0][0] * G.R[1][1] - G.R[0][1] * G.R[1][0];
-        detl = Rl[0][0] * Rl[1][1] - Rl[0][1] * Rl[1][0];
-        const double id = 1.0 / G.det;
-        G.Rinv[0][0] = G.R[1][1] * id;  G.Rinv[0][1] = -G.R[0][1] * id;
-        G.Rinv[1][0] = -G.R[1][0] * id; G.Rinv[1][1] = G.R[0][0] * id;
-    } else {
-        const double (*R)[3] = G.R;
-        const double c00 = R[1][1] * R[2][2] - R[1][2] * R[2][1];
-        const double c01 = R[1][2] * R[2][0] - R[1][0] * R[2][2];
-        const double c02 = R[1][0] * R[2][1] - R[1][1] * R[2][0];
-        G.det = R[0][0] * c00 + R[0][1] * c01 + R[0][2] * c02;
-        detl = Rl[0][0] * (Rl[1][1] * Rl[2][2] - Rl[1][2] * Rl[2][1]) -
-               Rl[0][1] * (Rl[1][0] * Rl[2][2] - Rl[1][2] * Rl[2][0]) +
-               Rl[0][2] * (Rl[1][0] * Rl[2][1] - Rl[1][1] * Rl[2][0]);
-        const double id = 1.0 / G.det;
-        G.Rinv[0][0] = c00 * id;
-        G.Rinv[1][0] = c01 * id;
-        G.Rinv[2][0] = c02 * id;
-        G.Rinv[0][1] = (R[0][2] * R[2][1] - R[0][1] * R[2][2]) * id;
-        G.Rinv[1][1] = (R[0][0] * R[2][2] - R[0][2] * R[2][0]) * id;
-        G.Rinv[2][1] = (R[0][1] * R[2][0] - R[0][0] * R[2][1]) * id;
-        G.Rinv[0][2] = (R[0][1] * R[1][2] - R[0][2] * R[1][1]) * id;
-        G.Rinv[1][2] = (R[0][2] * R[1][0] - R[0][0] * R[1][2]) * id;
-        G.Rinv[2][2] = (R[0][0] * R[1][1] - R[0][1] * R[1][0]) * id;
-    }
-    if (bad && G.valid && !(G.det * (double)detl > 0.0)) atomicOr(bad, 1);   // E_DEGENERATE_ELEMENT
-    return G;
-}
-
-// coefficient components at physical point x: isotropic -> out[0] = m;
-// tensor -> upper triangle row-major (2D: 3, 3D: 6 values)
-__device__ void coef_eval(int kind, const double* P, const double* per_cell, int64_t cell, int d,
-                          const double* x, double* out) {
-    switch (kind) {
-        case DOGIP_COEF_CONST: out[0] = P[0]; return;
-        case DOGIP_COEF_PER_CELL: out[0] = per_cell[cell]; return;
-        case DOGIP_COEF_SINCOS2D:
-            out[0] = P[0] + P[1] * sin(2.0 * M_PI * x[0]) * cos(2.0 * M_PI * x[1]);
-            return;
-        case DOGIP_COEF_TANH_RADIAL: {
-            double r2 = 0.0;
-            for (int a = 0; a < d; ++a) { const double t = x[a] - P[4 + a]; r2 += t * t; }
-            out[0] = P[0] + P[1] * tanh(P[2] * (sqrt(r2) - P[3]));
-            return;
-        }
-        case DOGIP_COEF_ANISO_FOURIER: {
-            const int n = (int)P[3];
-            const double* kap = P + 4;
-            const double* phi = P + 4 + 3 * n;
-            const double* cc = P + 4 + 6 * n;
-            double w[3] = {0.0, 0.0, 0.0};
-            for (int m = 0; m < n; ++m) {
-                const double arg = 2.0 * M_PI * (x[0] * kap[3 * m] + x[1] * kap[3 * m + 1] + x[2] * kap[3 * m + 2]);
-                for (int i = 0; i < 3; ++i) w[i] += cc[3 * m + i] * cos(arg + phi[3 * m + i]);
-            }
-            double R[3][3];
-            const double t = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
-            if (t < 1e-12) {
-                R[0][0] = 1; R[0][1] = -w[2]; R[0][2] = w[1];
-                R[1][0] = w[2]; R[1][1] = 1; R[1][2] = -w[0];
-                R[2][0] = -w[1]; R[2][1] = w[0]; R[2][2] = 1;
-            } else {
-                const double k0 = w[0] / t, k1 = w[1] / t, k2 = w[2] / t;
-                const double K[3][3] = {{0, -k2, k1}, {k2, 0, -k0}, {-k1, k0, 0}};
-                const double st = sin(t), ct1 = 1.0 - cos(t);
-                for (int a = 0; a < 3; ++a)
-                    for (int b = 0; b < 3; ++b) {
-                        double k2ab = 0.0;
-                        for (int c = 0; c < 3; ++c) k2ab += K[a][c] * K[c][b];
-                        R[a][b] = (a == b ? 1.0 : 0.0) + st * K[a][b] + ct1 * k2ab;
-                    }
-            }
-            int o = 0;
-            for (int a = 0; a < 3; ++a)
-                for (int b = a; b < 3; ++b) {
-                    double s = 0.0;
-                    for (int c = 0; c < 3; ++c) s += R[a][c] * P[c] * R[b][c];
-                    out[o++] = s;
-                }
-            return;
-        }
-        case DOGIP_COEF_CONST_TENSOR: {
-            int o = 0;
-            for (int a = 0; a < d; ++a)
-                for (int b = a; b < d; ++b) out[o++] = P[a * d + b];
-            return;
-        }
-    }
-}
-
-__device__ __forceinline__ bool coef_ok(int ncomp, int d, const double* c) {
-    if (ncomp == 1) return c[0] > 0.0;
-    return d == 2 ? (c[0] > 0.0 && c[2] > 0.0) : (c[0] > 0.0 && c[3] > 0.0 && c[5] > 0.0);
-}
 
 // 1. C[(e*ncomp + c)*nq + q] = |det| w_q M_c(x_q)
 __global__ void quad_coef_kernel(WeightsArgs a, int64_t e0, int64_t nb) {

@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--out", default=None)
     ap.add_argument("--iso", action="store_true", help="also the isotropic compressed EL storage")
+    ap.add_argument("--qp", action="store_true", help="also the quadrature-point matrix-free comparator")
     args = ap.parse_args()
     rows = []
     for name in args.configs.split(","):
@@ -63,6 +64,8 @@ def main():
             variants.append((0, 2))
         if args.iso and 0 in forms:
             variants.append((0, 3))
+        if args.qp:
+            variants += [(f, 4) for f in forms]
         for form, storage in variants:
             op = Operator(mesh, form, coef, storage=storage)
             oi = op.info
@@ -75,11 +78,14 @@ def main():
             alg = 8 * nw * c.n_elem + 16 * c.ndof
             if storage == 2:                      # global W vector read once (Theorem 1)
                 alg = oi["weight_bytes"] + 16 * c.ndof
+            if storage == 4:                      # comparator: no stored operator data
+                alg = 16 * c.ndof
             b = op.load_vector(1.0, dirichlet=dirichlet)
             x = torch.zeros_like(b)
             op.cg(b, x, maxit=-3, dirichlet=dirichlet)
             r = op.cg(b, x, maxit=-n, dirichlet=dirichlet, resume=True)
-            row = {"config": name, "form": ["WP", "EL", "EL-iso", "WP-glob", "WP-pair"][form if storage == 0 else storage + 1],
+            row = {"config": name, "form": (["WP", "EL", "EL-iso", "WP-glob", "WP-pair"][form if storage == 0 else storage + 1]
+                             if storage != 4 else ["WP-qp", "EL-qp"][form]),
                    "d": c.d, "N": c.N, "p": c.p, "flops_per_elem": oi["flops_per_elem"],
                    "fp64_TFs": oi["flops_per_elem"] * c.n_elem / t_apply / 1e12,
                    "n_elem": c.n_elem, "ndof": c.ndof, "W_T": oi["W_T"], "n_c": oi["n_c"],

@@ -452,3 +452,71 @@ def test_pair_storage_errors():
     with pytest.raises(DogipError) as ei:
         Operator(m, 1, TANH3, storage=3)
     assert ei.value.code == -10
+
+
+# Quadrature-point matrix-free comparator (DOGIP_STORE_QP, "alternative approaches" P:61-75)
+QP_CASES = [(d, p, f) for d in (2, 3) for p in (1, 2, 3, 4) for f in (0, 1)]
+
+
+@pytest.mark.parametrize("d,p,form", QP_CASES)
+def test_qp_comparator_matches_oracle(d, p, form):
+    """Same contract rule Q as the DoGIP weights -> the same Galerkin matrix A: the
+    on-the-fly quadrature apply matches the assembled A (smooth, point-evaluated
+    coefficients incl. the rotated anisotropic tensor, jittered meshes, ragged x-blocks)
+    and the DoGIP apply; with Dirichlet rows for EL."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    N = {2: 35, 3: 4}[d] if p <= 2 else {2: 9, 3: 3}[d]
+    coef = coef_for(d, form, "smooth")
+    verts = jitter_verts(d, N)
+    m = Mesh(d, N, p, verts)
+    op = Operator(m, form, coef, storage=4)
+    assert op.info["storage"] == 4 and op.info["weight_bytes"] == 0
+    ed = oa.build(d, N, p, verts)
+    A = oa.assemble_csr(ed, form, coef)
+    u = u_vector(ed.ndof, 0)
+    ut = torch.from_numpy(u).cuda()
+    y = op.apply(ut).cpu().numpy()
+    assert relerr(y, A @ u) <= TOL
+    yd = Operator(m, form, coef).apply(ut).cpu().numpy()
+    assert relerr(y, yd) <= TOL
+    if form == 1:
+        bmask = boundary_mask(d, N, p)
+        AD = oa.dirichlet_matrix(A, bmask)
+        yq = op.apply(ut, dirichlet=True).cpu().numpy()
+        assert relerr(yq, AD @ u) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C4", "C5", "C3"])
+def test_qp_comparator_full_size_sampled(name):
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config(name)
+    coef, verts = c.coefficient(), c.vertices()
+    m = Mesh(c.d, c.N, c.p, verts)
+    form = c.forms[0]
+    op = Operator(m, form, coef, storage=4)
+    u = c.u()
+    y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
+    rows = np.unique(np.random.default_rng(19).integers(0, c.ndof, 20))
+    ref = oa.apply_rows_sampled(c.d, c.N, c.p, verts, form, coef, u, rows)
+    assert np.abs(y[rows] - ref).max() / np.abs(y).max() <= TOL
+
+
+def test_qp_comparator_cg_and_errors():
+    torch = _torch()
+    from paper_1710_09913_b200.api import DogipError, Mesh, Operator
+    c = get_config("C1")
+    coef = c.coefficient()
+    m = Mesh(2, c.N, c.p)
+    op = Operator(m, 1, coef, storage=4)
+    b = op.load_vector(1.0, dirichlet=True)
+    x = torch.zeros_like(b)
+    res = op.cg(b, x, rtol=1e-10, dirichlet=True)
+    ed = oa.build(2, c.N, c.p)
+    AD = oa.dirichlet_matrix(oa.assemble_csr(ed, 1, coef), boundary_mask(2, c.N, c.p))
+    bn, xn = b.cpu().numpy(), x.cpu().numpy()
+    assert res["status"] == "OK"
+    assert np.linalg.norm(bn - AD @ xn) / np.linalg.norm(bn) <= 2e-10
+    with pytest.raises(DogipError):
+        op.export_weights()
