@@ -249,7 +249,11 @@ int dogip_load_vector(dogip_op op, double f, double* b, unsigned flags, void* st
  * iterations (maxit < 0: run exactly -maxit iterations, no convergence test --
  * benchmarking).  b, x: device, ndof_local.  Dots run over owned DoFs and are
  * all-reduced.  Synchronises `stream`.  Returns DOGIP_OK, DOGIP_NOT_CONVERGED
- * or DOGIP_E_BREAKDOWN (also in res->status).
+ * or DOGIP_E_BREAKDOWN (also in res->status).  Single rank, maxit > 0: the
+ * iterations run as one CUDA graph (conditional WHILE node around one iteration,
+ * device-side stopping test, no host round trip per iteration; built once per
+ * (x, flags, rtol, maxit, stream) and cached in the op, outside the timed
+ * res->seconds); environment DOGIP_CG_NO_GRAPH=1 selects the host-driven loop.
  */
 int dogip_cg(dogip_op op, const double* b, double* x, double rtol, int maxit, unsigned flags,
              void* stream, dogip_cg_result* res);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -81,6 +82,12 @@ struct dogip_op_s {
     double *q_pts = nullptr, *q_wts = nullptr, *q_phi = nullptr, *q_dphi = nullptr, *q_params = nullptr,
            *q_cell = nullptr;
     int q_kind = 0, q_ncomp = 1, q_nq = 0;
+    // graph-captured CG loop (single rank): conditional WHILE node around one iteration
+    cudaGraph_t cg_graph = nullptr;
+    cudaGraphExec_t cg_exec = nullptr;
+    int* cg_it = nullptr;
+    cudaStream_t cap_stream = nullptr;   // capture stream (the legacy default stream cannot capture)
+    struct { const double* x = nullptr; unsigned flags = 0; double rtol = 0.0; int maxit = 0; cudaStream_t st = nullptr; } cg_key;
     // pipelined host-buffer apply: copy-in / copy-out streams, one event pair per chunk
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     std::vector<cudaEvent_t> ev_in, ev_done;
@@ -521,6 +528,10 @@ extern "C" void dogip_op_destroy(dogip_op op) {
     cudaFree(op->d_offw);
     for (double* x : {op->q_pts, op->q_wts, op->q_phi, op->q_dphi, op->q_params, op->q_cell}) cudaFree(x);
     if (op->h_scal) cudaFreeHost(op->h_scal);
+    if (op->cg_exec) cudaGraphExecDestroy(op->cg_exec);
+    if (op->cg_graph) cudaGraphDestroy(op->cg_graph);
+    cudaFree(op->cg_it);
+    if (op->cap_stream) cudaStreamDestroy(op->cap_stream);
     for (cudaEvent_t e : op->ev_in) cudaEventDestroy(e);
     for (cudaEvent_t e : op->ev_done) cudaEventDestroy(e);
     if (op->s_h2d) cudaStreamDestroy(op->s_h2d);
@@ -750,6 +761,66 @@ static int allreduce_scalar(dogip_mesh_s* m, double* s, cudaStream_t st) {
 
 extern "C" int64_t dogip_kernel_launches(void) { return (int64_t)g_launches.load(); }
 
+// The CG iterations of a solve as one CUDA graph: a conditional WHILE node whose body is
+// one iteration (apply with fused p.q, r update + r.r, x/p update, cg_control), so the
+// loop runs without a host round trip per iteration; cg_control sets the condition.
+// Single rank only (the multi-rank loop all-reduces through NCCL between kernels).
+// Rebuilt when x, the flags, rtol, maxit or the stream change.
+static int cg_graph_build(dogip_op op, double* x, double rtol, int maxit, unsigned aflags, cudaStream_t st) {
+    dogip_mesh_s* m = op->m;
+    const int64_t n = m->geo.ndof;
+    dogip_mesh_info_t info;
+    dogip_mesh_info(m, &info);
+    if (!op->cg_it) CK(cudaMalloc(&op->cg_it, sizeof(int)));
+    if (!op->dotp) {
+        CK(cudaMalloc(&op->dotp, sizeof(double) * 3 * APPLY_MAX_WARPS));
+        CK(cudaMalloc(&op->bpart, sizeof(double) * RED_BLOCKS));
+    }
+    auto& k = op->cg_key;
+    if (!op->cg_exec || k.x != x || k.flags != aflags || k.rtol != rtol || k.maxit != maxit || k.st != st) {
+        if (op->cg_exec) { cudaGraphExecDestroy(op->cg_exec); op->cg_exec = nullptr; }
+        if (op->cg_graph) { cudaGraphDestroy(op->cg_graph); op->cg_graph = nullptr; }
+        CK(cudaGraphCreate(&op->cg_graph, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, op->cg_graph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, op->cg_graph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        if (!op->cap_stream) CK(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t cs = op->cap_stream;
+        CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        int rc = apply_impl(op, op->pv, op->q, aflags, cs, op->scal + S_PQ);     // q = A p, p.q fused
+        cudaError_t ce = cudaSuccess;
+        if (rc >= 0) ce = launch_cg_r(op->r, op->q, n, info.owned_begin, info.owned_end, op->scal, op->partials, cs);
+        if (rc >= 0 && ce == cudaSuccess) ce = launch_cg_px(x, op->pv, op->r, n, op->scal, cs);
+        if (rc >= 0 && ce == cudaSuccess) ce = launch_cg_control(op->scal, op->cg_it, rtol, maxit, h, cs);
+        cudaGraph_t captured = nullptr;
+        const cudaError_t ee = cudaStreamEndCapture(cs, &captured);
+        if (rc < 0) return rc;
+        CK(ce);
+        CK(ee);
+        CK(cudaGraphInstantiate(&op->cg_exec, op->cg_graph, 0));
+        k.x = x; k.flags = aflags; k.rtol = rtol; k.maxit = maxit; k.st = st;
+    }
+    return DOGIP_OK;
+}
+
+static int cg_graph_run(dogip_op op, cudaStream_t st, int* iters) {
+    CK(cudaMemsetAsync(op->cg_it, 0, sizeof(int), st));
+    CK(cudaGraphLaunch(op->cg_exec, st));
+    CK(cudaMemcpyAsync(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
+    int it = 0;
+    CK(cudaMemcpyAsync(&it, op->cg_it, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *iters = it;
+    return DOGIP_OK;
+}
+
 extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, int maxit, unsigned flags,
                         void* stream, dogip_cg_result* res) {
     if (!op || !b || !x || !res) return fail(DOGIP_E_INVALID_ARG, "null argument");
@@ -787,6 +858,9 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
         aev.resize(2 * (size_t)nit);
         for (auto& e : aev) CK(cudaEventCreate(&e));
     }
+    // the graph-captured loop is built (or reused) before the timed region
+    const bool graph_ok = !bench && nit > 0 && m->nranks == 1 && std::getenv("DOGIP_CG_NO_GRAPH") == nullptr;
+    if (graph_ok) RET(cg_graph_build(op, x, rtol, nit, aflags, st));
     CK(cudaEventRecord(t0, st));
     if (!resume) {
         // r = b - A x ; p = r
@@ -811,7 +885,14 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
         }
     }
     int it = 0, status = DOGIP_OK;
-    while (true) {
+    const bool graph = graph_ok && !(std::sqrt(rr) <= rtol * bnorm);
+    if (graph) {
+        RET(cg_graph_run(op, st, &it));
+        rr = op->h_scal[S_RR];
+        if (!(op->h_scal[S_PQ] > 0.0)) status = DOGIP_E_BREAKDOWN;
+        else if (!(std::sqrt(rr) <= rtol * bnorm)) status = DOGIP_NOT_CONVERGED;
+    }
+    while (!graph) {
         if (!bench && std::sqrt(rr) <= rtol * bnorm) break;
         if (it >= nit) { status = bench ? DOGIP_OK : DOGIP_NOT_CONVERGED; break; }
         if (bench) CK(cudaEventRecord(aev[2 * it], st));

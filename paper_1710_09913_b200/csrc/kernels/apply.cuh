@@ -153,5 +153,8 @@ cudaError_t launch_cg_r(double* r, const double* q, int64_t n, int64_t i0, int64
 cudaError_t launch_cg_px(double* x, double* p, const double* r, int64_t n, double* scal, cudaStream_t st);
 
 enum CgScal { S_RR = 0, S_PQ = 1, S_RRNEW = 2, S_BB = 3, S_COUNT = 8 };
+// graph-captured CG: ++*it_d; conditional = !(converged || breakdown || *it_d >= maxit)
+cudaError_t launch_cg_control(const double* scal, int* it_d, double rtol, int maxit, cudaGraphConditionalHandle h,
+                              cudaStream_t st);
 
 }  // namespace dogip

@@ -138,6 +138,17 @@ __global__ void __launch_bounds__(RED_THREADS) cg_p_kernel(double* __restrict__ 
 
 __global__ void shift_rr_kernel(double* scal) { scal[S_RR] = scal[S_RRNEW]; }
 
+// device-side loop control of the graph-captured CG (conditional WHILE node): count the
+// iteration, stop on convergence ||r|| <= rtol ||b||, breakdown p.q <= 0 or maxit
+__global__ void cg_control_kernel(const double* scal, int* it_d, double rtol, int maxit,
+                                  cudaGraphConditionalHandle h) {
+    const int it = *it_d + 1;
+    *it_d = it;
+    const bool breakdown = !(scal[S_PQ] > 0.0);
+    const bool conv = sqrt(scal[S_RR]) <= rtol * sqrt(scal[S_BB]);
+    cudaGraphSetConditional(h, (!breakdown && !conv && it < maxit) ? 1u : 0u);
+}
+
 __global__ void axpby_kernel(double* y, const double* x, double a, double b, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         y[i] = a * x[i] + b * y[i];
@@ -337,6 +348,13 @@ cudaError_t launch_cg_p(double* p, const double* r, int64_t n, double* scal, cud
     cg_p_kernel<<<RED_BLOCKS, RED_THREADS, 0, st>>>(p, r, n, scal);
     shift_rr_kernel<<<1, 1, 0, st>>>(scal);
     count_launches(2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_control(const double* scal, int* it_d, double rtol, int maxit, cudaGraphConditionalHandle h,
+                              cudaStream_t st) {
+    cg_control_kernel<<<1, 1, 0, st>>>(scal, it_d, rtol, maxit, h);
+    count_launches(1);
     return cudaGetLastError();
 }
 

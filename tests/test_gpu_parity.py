@@ -520,3 +520,43 @@ def test_qp_comparator_cg_and_errors():
     assert np.linalg.norm(bn - AD @ xn) / np.linalg.norm(bn) <= 2e-10
     with pytest.raises(DogipError):
         op.export_weights()
+
+
+@pytest.mark.parametrize("name,form,N", [("C1", 1, 16), ("C3", 1, 6), ("C5", 0, 5)])
+def test_cg_graph_matches_host_loop(name, form, N, monkeypatch):
+    """The graph-captured CG (conditional WHILE node, device-side stopping test) runs
+    the same iterations as the host-driven loop: same count, same x to rounding, and
+    a true residual within 2 rtol; re-running reuses the cached graph."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config(name).with_size(N)
+    m = Mesh(c.d, c.N, c.p, c.vertices())
+    op = Operator(m, form, c.coefficient())
+    dirichlet = form == 1
+    tol = 1e-10
+    b = op.load_vector(1.0, dirichlet=dirichlet)
+    xg = torch.zeros_like(b)
+    rg = op.cg(b, xg, rtol=tol, dirichlet=dirichlet)
+    xg2 = torch.zeros_like(b)
+    rg2 = op.cg(b, xg2, rtol=tol, dirichlet=dirichlet)     # cached graph (different x -> rebuilt)
+    monkeypatch.setenv("DOGIP_CG_NO_GRAPH", "1")
+    xh = torch.zeros_like(b)
+    rh = op.cg(b, xh, rtol=tol, dirichlet=dirichlet)
+    assert rg["status"] == rh["status"] == rg2["status"] == "OK"
+    # rounding-level differences (below) can move the stopping test by an iteration
+    assert abs(rg["iters"] - rh["iters"]) <= 2 and abs(rg2["iters"] - rh["iters"]) <= 2
+    # the scatter's atomics make two CG runs differ at rounding level (reading L25), which
+    # the iteration amplifies by up to ~cond(A): compare to 100 rtol, not bitwise
+    assert relerr(xg.cpu().numpy(), xh.cpu().numpy()) <= 100 * tol
+    assert relerr(xg2.cpu().numpy(), xh.cpu().numpy()) <= 100 * tol
+    ed = oa.build(c.d, c.N, c.p, c.vertices())
+    A = oa.assemble_csr(ed, form, c.coefficient())
+    if dirichlet:
+        A = oa.dirichlet_matrix(A, boundary_mask(c.d, c.N, c.p))
+    bn, xn = b.cpu().numpy(), xg.cpu().numpy()
+    assert np.linalg.norm(bn - A @ xn) / np.linalg.norm(bn) <= 2 * tol
+    # maxit reached inside the graph -> NOT_CONVERGED with exactly maxit iterations
+    monkeypatch.delenv("DOGIP_CG_NO_GRAPH")
+    x3 = torch.zeros_like(b)
+    r3 = op.cg(b, x3, rtol=1e-30, maxit=7, dirichlet=dirichlet)
+    assert r3["status"] == "NOT_CONVERGED" and r3["iters"] == 7
