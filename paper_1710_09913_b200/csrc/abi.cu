@@ -434,7 +434,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     }
     const bool direct = coeff->kind == DOGIP_COEF_CONST || coeff->kind == DOGIP_COEF_PER_CELL ||
                         coeff->kind == DOGIP_COEF_CONST_TENSOR;
-    int64_t batch = (int64_t)(256ll << 20) / (8ll * ncomp * std::max(nq, WT));
+    int64_t batch = (int64_t)(1024ll << 20) / (8ll * ncomp * std::max(nq, WT));   // 1 GB of scratch
     batch = std::max<int64_t>(TILE, batch / TILE * TILE);
     a.batch = batch;
     if (!direct) {

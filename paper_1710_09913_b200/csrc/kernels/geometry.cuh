@@ -17,19 +17,34 @@ struct Geo {
     bool valid;
 };
 
-// Simplex vertex offsets of one cell (reading L3): 2D right split, 3D Kuhn.
-__device__ __forceinline__ void simplex_offset(int d, int s, int v, int o[3]) {
+// Simplex vertex offsets of one cell (reading L3): 2D right split, 3D Kuhn (vertex v
+// = sum of the first v axes of permutation s, permutations in lexicographic order).
+// Compile-time D and register arithmetic only (no dynamically indexed local arrays).
+template <int D>
+__device__ __forceinline__ void simplex_offset(int s, int v, int o[3]) {
     o[0] = o[1] = o[2] = 0;
     if (v == 0) return;
-    if (d == 2) {
+    if constexpr (D == 2) {
         if (s == 0) { o[0] = 1; o[1] = (v == 2); }
         else { o[1] = 1; o[0] = (v == 1); }
-        return;
+    } else {
+        // axes of permutation s packed 2 bits each, 6 bits per permutation:
+        // {0,1,2},{0,2,1},{1,0,2},{1,2,0},{2,0,1},{2,1,0}
+        constexpr unsigned long long PACK = (0ull | 1ull << 2 | 2ull << 4) | (0ull | 2ull << 2 | 1ull << 4) << 6 |
+                                            (1ull | 0ull << 2 | 2ull << 4) << 12 | (1ull | 2ull << 2 | 0ull << 4) << 18 |
+                                            (2ull | 0ull << 2 | 1ull << 4) << 24 | (2ull | 1ull << 2 | 0ull << 4) << 30;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const int ax = (int)((PACK >> (6 * s + 2 * i)) & 3ull);
+            const int add = i < v ? 1 : 0;
+            o[0] += ax == 0 ? add : 0;
+            o[1] += ax == 1 ? add : 0;
+            o[2] += ax == 2 ? add : 0;
+        }
     }
-    const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-    for (int i = 0; i < v; ++i) o[perms[s][i]] += 1;
 }
 
+template <int D>
 __device__ __forceinline__ Geo element_geo(const SlabGeo& g, const double* verts, int64_t eK, int* bad) {
     Geo G;
     const int64_t tile = eK / TILE;
@@ -37,37 +52,47 @@ __device__ __forceinline__ Geo element_geo(const SlabGeo& g, const double* verts
     const TileCoord tc = tile_coord(g, tile);
     const int ci = tc.ci0 + lane;
     G.valid = ci < g.Nx;
-    const int d = g.d;
     int64_t c[3] = {ci, tc.cj, tc.ck};
-    if (d == 2) c[1] += g.zoff; else c[2] += g.zoff;
+    if (D == 2) c[1] += g.zoff; else c[2] += g.zoff;
     if (!G.valid) c[0] = 0;
-    G.cell = d == 2 ? c[0] + (int64_t)g.N * c[1] : c[0] + (int64_t)g.N * (c[1] + (int64_t)g.N * c[2]);
+    G.cell = D == 2 ? c[0] + (int64_t)g.N * c[1] : c[0] + (int64_t)g.N * (c[1] + (int64_t)g.N * c[2]);
     const int64_t M = g.N + 1;
-    double X[4][3];
-    int lat[4][3];
-    for (int v = 0; v <= d; ++v) {
+    double X[D + 1][D];
+    int lat[D + 1][D];
+#pragma unroll
+    for (int v = 0; v <= D; ++v) {
         int o[3];
-        simplex_offset(d, tc.s, v, o);
+        simplex_offset<D>(tc.s, v, o);
         int64_t vid = 0, mul = 1;
-        for (int a = 0; a < d; ++a) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
             lat[v][a] = o[a];
             vid += (c[a] + o[a]) * mul;
             mul *= M;
         }
-        for (int a = 0; a < d; ++a)
-            X[v][a] = verts ? verts[vid * d + a] : (double)(c[a] + o[a]) / (double)g.N;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+            X[v][a] = verts ? verts[vid * D + a] : (double)(c[a] + o[a]) / (double)g.N;
     }
-    for (int a = 0; a < 3; ++a)
-        for (int b = 0; b < 3; ++b) G.R[a][b] = (a == b) ? 1.0 : 0.0;
-    for (int a = 0; a < d; ++a) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        G.S[a] = 0.0;
+#pragma unroll
+        for (int b = 0; b < 3; ++b) { G.R[a][b] = (a == b) ? 1.0 : 0.0; G.Rinv[a][b] = (a == b) ? 1.0 : 0.0; }
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
         G.S[a] = X[0][a];
-        for (int b = 0; b < d; ++b) G.R[a][b] = X[b + 1][a] - X[0][a];   // columns v_b - v_0
+#pragma unroll
+        for (int b = 0; b < D; ++b) G.R[a][b] = X[b + 1][a] - X[0][a];   // columns v_b - v_0
     }
     int Rl[3][3];
-    for (int a = 0; a < d; ++a)
-        for (int b = 0; b < d; ++b) Rl[a][b] = lat[b + 1][a] - lat[0][a];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) Rl[a][b] = lat[b + 1][a] - lat[0][a];
     int detl;
-    if (d == 2) {
+    if constexpr (D == 2) {
         G.det = G.R[0][0] * G.R[1][1] - G.R[0][1] * G.R[1][0];
         detl = Rl[0][0] * Rl[1][1] - Rl[0][1] * Rl[1][0];
         const double id = 1.0 / G.det;
@@ -99,8 +124,10 @@ __device__ __forceinline__ Geo element_geo(const SlabGeo& g, const double* verts
 
 // coefficient components at physical point x: isotropic -> out[0] = m;
 // tensor -> upper triangle row-major (2D: 3, 3D: 6 values)
-__device__ __forceinline__ void coef_eval(int kind, const double* P, const double* per_cell, int64_t cell, int d,
-                          const double* x, double* out) {
+template <int D>
+__device__ __forceinline__ void coef_eval(int kind, const double* P, const double* per_cell, int64_t cell,
+                                          const double* x, double* out) {
+    constexpr int d = D;
     switch (kind) {
         case DOGIP_COEF_CONST: out[0] = P[0]; return;
         case DOGIP_COEF_PER_CELL: out[0] = per_cell[cell]; return;
@@ -109,6 +136,7 @@ __device__ __forceinline__ void coef_eval(int kind, const double* P, const doubl
             return;
         case DOGIP_COEF_TANH_RADIAL: {
             double r2 = 0.0;
+#pragma unroll
             for (int a = 0; a < d; ++a) { const double t = x[a] - P[4 + a]; r2 += t * t; }
             out[0] = P[0] + P[1] * tanh(P[2] * (sqrt(r2) - P[3]));
             return;
@@ -151,7 +179,9 @@ __device__ __forceinline__ void coef_eval(int kind, const double* P, const doubl
         }
         case DOGIP_COEF_CONST_TENSOR: {
             int o = 0;
+#pragma unroll
             for (int a = 0; a < d; ++a)
+#pragma unroll
                 for (int b = a; b < d; ++b) out[o++] = P[a * d + b];
             return;
         }

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(QP_THREADS) qp_apply_kernel(QpArgs a, const Ap
         const TileCoord tc = tile_coord(g, tile);
         const int ci = tc.ci0 + lane;
         if (ci >= g.Nx) continue;
-        const Geo G = element_geo(g, a.verts, eK, nullptr);
+        const Geo G = element_geo<D>(g, a.verts, eK, nullptr);
         const int64_t base = (int64_t)g.p * (ci + g.sy * tc.cj + g.sz * tc.ck);
         const int v1 = tab.vstr[tc.s][0], v2 = tab.vstr[tc.s][1], v3 = D == 3 ? tab.vstr[tc.s][2] : 0;
         uint64_t skip = 0;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(QP_THREADS) qp_apply_kernel(QpArgs a, const Ap
         }
         const double adet = fabs(G.det);
         double cc[6];
-        if (cellconst) coef_eval(a.kind, a.params, a.per_cell, G.cell, D, G.S, cc);
+        if (cellconst) coef_eval<D>(a.kind, a.params, a.per_cell, G.cell, G.S, cc);
         if constexpr (F == 0) {
             // WP (eq:bilf_gp P:189): h_q = w_q |det| m(x_q) u(x_q)
             for (int q = 0; q < a.nq; ++q) {
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(QP_THREADS) qp_apply_kernel(QpArgs a, const Ap
 #pragma unroll
                         for (int c = 0; c < D; ++c) x[r] += G.R[r][c] * __ldg(a.qp + q * D + c);
                     double cv[6];
-                    coef_eval(a.kind, a.params, a.per_cell, G.cell, D, x, cv);
+                    coef_eval<D>(a.kind, a.params, a.per_cell, G.cell, x, cv);
                     m = cv[0];
                 }
                 const double h = __ldg(a.qw + q) * adet * m * v;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(QP_THREADS) qp_apply_kernel(QpArgs a, const Ap
 #pragma unroll
                         for (int c = 0; c < D; ++c) x[r] += G.R[r][c] * __ldg(a.qp + q * D + c);
                     double cv[6];
-                    coef_eval(a.kind, a.params, a.per_cell, G.cell, D, x, cv);
+                    coef_eval<D>(a.kind, a.params, a.per_cell, G.cell, x, cv);
                     congruence(cv, K);
                 }
                 const double wq = __ldg(a.qw + q);

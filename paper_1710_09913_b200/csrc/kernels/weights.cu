@@ -5,7 +5,7 @@
 // with the collapsed Gauss-Jacobi rule Q (reading L10).  Three steps per batch
 // of elements (K-order = apply-kernel tile order):
 //   1. quad_coef : C[e, c, q] = |det R_T| w_q M_c(F_T xq)      (c = coefficient component)
-//   2. gemm      : Abar[e, c, j] = sum_q C[e, c, q] Phi[q, j]   (smem-tiled FP64 GEMM)
+//   2. gemm      : Abar[e, c, j] = sum_q C[e, c, q] Phi[q, j]   (smem-tiled FP64 DMMA GEMM)
 //   3. finalize  : congruence with Rinv_T (EL) and the tile-major store [tile][j*NC+c][lane]
 // Cell-constant coefficients skip 1-2: Abar = |det R_T| M_T s_j, s_j = sum_q w_q phi^W_j(xq).
 #include <cuda_runtime.h>
@@ -18,74 +18,128 @@
 namespace dogip {
 namespace {
 
-// 1. C[(e*ncomp + c)*nq + q] = |det| w_q M_c(x_q)
+// 1. CT[q][e*ncomp + c] = |det| w_q M_c(x_q)   (element index fastest: coalesced stores,
+//    and the GEMM's A operand read along M)
+template <int D>
 __global__ void quad_coef_kernel(WeightsArgs a, int64_t e0, int64_t nb) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= nb * a.nq) return;
-    const int64_t el = idx / a.nq;
-    const int q = (int)(idx % a.nq);
-    const Geo G = element_geo(a.geo, a.verts, e0 + el, a.bad_flag);
-    const int d = a.d;
-    double x[3] = {0, 0, 0};
-    for (int r = 0; r < d; ++r) {
-        x[r] = G.S[r];
-        for (int c = 0; c < d; ++c) x[r] += G.R[r][c] * a.qp[q * d + c];
+    // one thread per element (geometry once), looping over the points; for a fixed point
+    // consecutive threads write consecutive elements
+    const int64_t el = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (el >= nb) return;
+    const Geo G = element_geo<D>(a.geo, a.verts, e0 + el, a.bad_flag);
+    const double adet = G.valid ? fabs(G.det) : 0.0;
+    const int64_t M = nb * a.ncomp;
+    bool ok = true;
+    for (int q = 0; q < a.nq; ++q) {
+        double x[3] = {0, 0, 0};
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            x[r] = G.S[r];
+#pragma unroll
+            for (int c = 0; c < D; ++c) x[r] += G.R[r][c] * a.qp[q * D + c];
+        }
+        double cv[6];
+        coef_eval<D>(a.kind, a.params, a.per_cell, G.cell, x, cv);
+        ok = ok && coef_ok(a.ncomp, D, cv);
+        const double sc = adet * a.qw[q];
+        for (int c = 0; c < a.ncomp; ++c) a.scratch_c[(int64_t)q * M + el * a.ncomp + c] = sc * cv[c];
     }
-    double cv[6];
-    coef_eval(a.kind, a.params, a.per_cell, G.cell, d, x, cv);
-    if (G.valid && !coef_ok(a.ncomp, d, cv)) atomicOr(a.bad_flag, 2);
-    const double sc = G.valid ? fabs(G.det) * a.qw[q] : 0.0;
-    for (int c = 0; c < a.ncomp; ++c) a.scratch_c[(el * a.ncomp + c) * a.nq + q] = sc * cv[c];
+    if (G.valid && !ok) atomicOr(a.bad_flag, 2);
 }
 
-// 2. C (M x N) = A (M x K) * B (K x N), row-major, FP64, 64x64 tiles, 4x4 per thread
-constexpr int GB = 64, GK = 16;
-__global__ void __launch_bounds__(256) gemm_kernel(const double* __restrict__ A, const double* __restrict__ B,
+// 2. C (M x N) = A^T (K x M)^T * B (K x N), row-major, FP64 on the FP64 tensor path
+//    (mma.sync.aligned.m8n8k4.f64, DMMA -- sm_100a has no tcgen05 f64 kind): block tile
+//    64 (M) x 56 (N), 4 warps each owning 2 x 7 m8n8 accumulator tiles, K in steps of
+//    16 through padded shared memory (row stride 68 / 60 doubles: a fragment load is the
+//    optimal 2 wavefronts).  N = W_T: 165 (C5) -> 3 column blocks of 56 (2 % padding).
+constexpr int GBM = 64, GBN = 56, GK = 16, GPA = GBM + 4, GPB = GBN + 4;
+__device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(128) gemm_kernel(const double* __restrict__ AT, const double* __restrict__ B,
                                                    double* __restrict__ C, int64_t M, int N, int K) {
-    __shared__ double As[GK][GB + 1];
-    __shared__ double Bs[GK][GB + 1];
-    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    const int64_t m0 = (int64_t)blockIdx.x * GB;
-    const int n0 = blockIdx.y * GB;
-    double acc[4][4] = {};
-    for (int k0 = 0; k0 < K; k0 += GK) {
-        for (int i = threadIdx.x; i < GB * GK; i += 256) {
-            const int mm = i / GK, kk = i % GK;
+    __shared__ __align__(16) double As[GK][GPA];
+    __shared__ __align__(16) double Bs[GK][GPB];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t m0 = (int64_t)blockIdx.x * GBM;
+    const int n0 = blockIdx.y * GBN;
+    double acc[2][7][2] = {};
+    // register-staged double buffering: the next K slab's global loads are in flight
+    // while this slab's DMMAs run
+    constexpr int LA = GBM * GK / 128, LB = GBN * GK / 128;
+    double ra[LA], rb[LB];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int r = 0; r < LA; ++r) {
+            const int i = threadIdx.x + r * 128, kk = i / GBM, mm = i % GBM;
             const int64_t gm = m0 + mm;
-            As[kk][mm] = (gm < M && k0 + kk < K) ? A[gm * K + k0 + kk] : 0.0;
-            const int kb = i / GB, nn = i % GB;
-            Bs[kb][nn] = (k0 + kb < K && n0 + nn < N) ? B[(int64_t)(k0 + kb) * N + n0 + nn] : 0.0;
+            ra[r] = (gm < M && k0 + kk < K) ? AT[(int64_t)(k0 + kk) * M + gm] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < LB; ++r) {
+            const int i = threadIdx.x + r * 128, kb = i / GBN, nn = i % GBN;
+            rb[r] = (k0 + kb < K && n0 + nn < N) ? B[(int64_t)(k0 + kb) * N + n0 + nn] : 0.0;
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int r = 0; r < LA; ++r) {
+            const int i = threadIdx.x + r * 128;
+            As[i / GBM][i % GBM] = ra[r];
+        }
+#pragma unroll
+        for (int r = 0; r < LB; ++r) {
+            const int i = threadIdx.x + r * 128;
+            Bs[i / GBN][i % GBN] = rb[r];
+        }
+    };
+    load(0);
+    store();
+    __syncthreads();
+    for (int k0 = 0; k0 < K; k0 += GK) {
+        const bool more = k0 + GK < K;
+        if (more) load(k0 + GK);
+#pragma unroll
+        for (int ks = 0; ks < GK / 4; ++ks) {
+            const int kr = ks * 4 + (lane & 3);
+            double af[2], bf[7];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) af[mt] = As[kr][(warp * 2 + mt) * 8 + (lane >> 2)];
+#pragma unroll
+            for (int nt = 0; nt < 7; ++nt) bf[nt] = Bs[kr][nt * 8 + (lane >> 2)];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 7; ++nt) dmma_884(acc[mt][nt][0], acc[mt][nt][1], af[mt], bf[nt]);
         }
         __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < GK; ++kk) {
-            double av[4], bv[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        if (more) {
+            store();
+            __syncthreads();
         }
-        __syncthreads();
     }
-    for (int i = 0; i < 4; ++i)
-        for (int j = 0; j < 4; ++j) {
-            const int64_t gm = m0 + ty * 4 + i;
-            const int gn = n0 + tx * 4 + j;
-            if (gm < M && gn < N) C[gm * N + gn] = acc[i][j];
-        }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 7; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t gm = m0 + (warp * 2 + mt) * 8 + (lane >> 2);
+                const int gn = n0 + nt * 8 + 2 * (lane & 3) + h;
+                if (gm < M && gn < N) C[gm * N + gn] = acc[mt][nt][h];
+            }
 }
 
 // 3. congruence + tile-major store.  direct: cell-constant coefficient.
+template <int D>
 __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direct) {
     const int64_t el = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (el >= nb) return;
     const int64_t eK = e0 + el;
-    const Geo G = element_geo(a.geo, a.verts, eK, a.bad_flag);
-    const int d = a.d, WT = a.WT, NC = a.NC, nc = a.ncomp;
+    const Geo G = element_geo<D>(a.geo, a.verts, eK, a.bad_flag);
+    constexpr int d = D;
+    const int WT = a.WT, NC = a.NC, nc = a.ncomp;
     const int64_t tile = eK / TILE;
     const int lane = (int)(eK % TILE);
     double* out = a.out + (size_t)tile * a.tile_rows * TILE + lane;
@@ -95,7 +149,7 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
     double cconst[6] = {0, 0, 0, 0, 0, 0};
     if (direct) {
         double x[3] = {G.S[0], G.S[1], G.S[2]};
-        coef_eval(a.kind, a.params, a.per_cell, G.cell, d, x, cconst);
+        coef_eval<D>(a.kind, a.params, a.per_cell, G.cell, x, cconst);
         if (G.valid && !coef_ok(nc, d, cconst)) atomicOr(a.bad_flag, 2);
     }
     const double adet = fabs(G.det);
@@ -165,13 +219,14 @@ cudaError_t launch_weights(const WeightsArgs& a) {
     for (int64_t e0 = 0; e0 < nel; e0 += a.batch) {
         const int64_t nb = (nel - e0) < a.batch ? (nel - e0) : a.batch;
         if (!direct) {
-            const int64_t nthr = nb * a.nq;
-            quad_coef_kernel<<<(unsigned)((nthr + 255) / 256), 256, 0, a.stream>>>(a, e0, nb);
+            if (a.d == 2) quad_coef_kernel<2><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb);
+            else quad_coef_kernel<3><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb);
             const int64_t M = nb * a.ncomp;
-            dim3 grid((unsigned)((M + GB - 1) / GB), (unsigned)((a.WT + GB - 1) / GB));
-            gemm_kernel<<<grid, 256, 0, a.stream>>>(a.scratch_c, a.phiW, a.scratch_a, M, a.WT, a.nq);
+            dim3 grid((unsigned)((M + GBM - 1) / GBM), (unsigned)((a.WT + GBN - 1) / GBN));
+            gemm_kernel<<<grid, 128, 0, a.stream>>>(a.scratch_c, a.phiW, a.scratch_a, M, a.WT, a.nq);
         }
-        finalize_kernel<<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb, direct ? 1 : 0);
+        if (a.d == 2) finalize_kernel<2><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb, direct ? 1 : 0);
+        else finalize_kernel<3><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb, direct ? 1 : 0);
         count_launches(direct ? 1 : 3);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -220,11 +275,12 @@ cudaError_t launch_globalize(const SlabGeo& g, int WT, const double* wel, const 
 
 // ---------------------------------------------------------- load vector (K5)
 namespace {
+template <int D>
 __global__ void load_vector_kernel(SlabGeo g, const double* verts, const double* sV, int VT,
                                    const ApplyTables tab, double f, double* b) {
     const int64_t eK = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (eK >= g.ntiles * TILE) return;
-    const Geo G = element_geo(g, verts, eK, nullptr);
+    const Geo G = element_geo<D>(g, verts, eK, nullptr);
     if (!G.valid) return;
     const int64_t tile = eK / TILE;
     const int lane = (int)(eK % TILE);
@@ -240,7 +296,8 @@ cudaError_t launch_load_vector(const SlabGeo& g, int p, const double* verts, con
                                const ApplyTables* tab, double f, double* b, cudaStream_t st) {
     (void)p;
     const int64_t n = g.ntiles * TILE;
-    load_vector_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, verts, sV, VT, *tab, f, b);
+    if (g.d == 2) load_vector_kernel<2><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, verts, sV, VT, *tab, f, b);
+    else load_vector_kernel<3><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(g, verts, sV, VT, *tab, f, b);
     count_launches(1);
     return cudaGetLastError();
 }
