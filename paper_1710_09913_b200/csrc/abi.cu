@@ -143,6 +143,10 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
     g.Nz = d == 2 ? 1 : (int)L;
     g.nxb = (int)((N + TILE - 1) / TILE);
     g.ntiles = (int64_t)g.ns * g.nxb * g.Ny * g.Nz;
+    if (2 * g.ntiles >= (int64_t)1 << 31) {   // tile_coord's 32-bit arithmetic (half-tiles of PAIR)
+        delete m;
+        return fail(DOGIP_E_INVALID_SIZE, "invalid-size: more than 2^30 element tiles per rank");
+    }
     g.sy = M;
     g.sz = d == 3 ? M * M : 0;
     g.ndof = ipow(M, d - 1) * (p * L + 1);

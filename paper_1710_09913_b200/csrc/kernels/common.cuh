@@ -33,17 +33,22 @@ struct SlabGeo {
 struct TileCoord {
     int s, ci0, cj, ck;
 };
-__device__ __host__ inline TileCoord tile_coord(const SlabGeo& g, int64_t t) {
+// 32-bit unsigned arithmetic: a slab has < 2^31 tiles (dogip_mesh_setup rejects more),
+// and 64-bit division is ~5x the instructions -- it dominated tiny tiles (2D P1).
+__device__ __host__ inline TileCoord tile_coord(const SlabGeo& g, int64_t t64) {
     TileCoord c;
-    c.s = (int)(t % g.ns);
-    int64_t rest = t / g.ns;
-    const int xb = (int)(rest % g.nxb);
-    rest /= g.nxb;
+    const uint32_t t = (uint32_t)t64, ns = (uint32_t)g.ns, nxb = (uint32_t)g.nxb;
+    const uint32_t r1 = t / ns;
+    c.s = (int)(t - r1 * ns);
+    const uint32_t r2 = r1 / nxb;
+    const int xb = (int)(r1 - r2 * nxb);
     if (g.d == 3) {
-        c.cj = (int)(rest % g.Ny);
-        c.ck = (int)(rest / g.Ny);
+        const uint32_t ny = (uint32_t)g.Ny;
+        const uint32_t ck = r2 / ny;
+        c.cj = (int)(r2 - ck * ny);
+        c.ck = (int)ck;
     } else {
-        c.cj = (int)rest;
+        c.cj = (int)r2;
         c.ck = 0;
     }
     c.ci0 = xb * TILE;
