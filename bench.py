@@ -284,6 +284,35 @@ def run_product(args, cfg) -> None:
     t_e2e = torch.tensor([f0.elapsed_time(f1) * 1e-3 / ke], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    # secondary (not the headline): the isotropic compressed storage of the corollary
+    # P:411-428 on the same workload -- FP64-bound instead of HBM-bound
+    iso = None
+    if form == 1 and storage == 0 and coef.isotropic and not args.no_variants:
+        op.close()                      # free the full weights first (21 GB at N=1)
+        torch.cuda.empty_cache()
+        op2 = Operator(mesh, form, coef, storage=1)
+        y2 = torch.empty_like(b)
+        for _ in range(3):
+            op2.apply(b, y2, dirichlet=dirichlet)
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            op2.apply(b, y2, dirichlet=dirichlet)
+        g1.record(stream)
+        barrier()
+        ti = torch.tensor([g0.elapsed_time(g1) * 1e-3 / args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ti, op=dist.ReduceOp.MAX)
+        oi2 = op2.info
+        t_iso = ti.item()
+        iso = {"storage": "iso (a_{T,j} and G_T = R^-1 R^-T, P:411-428)", "apply_ms": t_iso * 1e3,
+               "value": info["ndof_global"] / t_iso / 1e9, "unit": UNIT,
+               "bound": "fp64", "fp64_tflops": oi2["flops_per_elem"] * info["n_elem_local"] / t_iso / 1e12,
+               "fp64_frac_of_measured_dfma": oi2["flops_per_elem"] * info["n_elem_local"] / t_iso / 1e12 / FP64_PEAK_TFLOPS,
+               "weights_ms": oi2["weights_ms"],
+               "alg_bytes_per_launch": 8 * (oi2["W_T"] + oi2["n_c"]) * info["n_elem_local"] + 16 * info["ndof_local"]}
+        op2.close()
     nbytes_vec = 8 * info["ndof_local"]
     tot_vec = torch.tensor([nbytes_vec], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -312,6 +341,8 @@ def run_product(args, cfg) -> None:
                               "streams when single-rank)"},
                "gpu_launches": int(launches),
                "clocks": clocks}
+        if iso:
+            out["variants"] = {"iso": iso}
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(cfg)
         print(json.dumps(out), flush=True)
@@ -328,6 +359,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the secondary ISO-storage measurement")
     ap.add_argument("--storage", default="full", choices=["full", "iso"],
                     help="EL weight storage: full symmetric blocks (P:443) or the isotropic "
                          "compression of the corollary P:411-428 (a_{T,j} R^-1 R^-T)")

@@ -674,7 +674,9 @@ static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_hos
     const int64_t tpl = g.ntiles / layers;
     const int64_t plane = g.d == 3 ? g.sz : g.sy;
     const int p = m->p;
-    const int K = (int)std::min<int64_t>(layers, 16);
+    int kmax = 16;                                   // chunks (DOGIP_HOST_CHUNKS overrides, A/B)
+    if (const char* e = std::getenv("DOGIP_HOST_CHUNKS")) kmax = std::max(1, std::atoi(e));
+    const int K = (int)std::min<int64_t>(layers, kmax);
     const bool dir = (flags & DOGIP_DIRICHLET_ZERO) != 0;
     if (!op->s_h2d) {
         CK(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking));
