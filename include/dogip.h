@@ -77,6 +77,12 @@ extern "C" {
 #define DOGIP_STORE_PAIR   3 /* WP only: the values of DOGIP_STORE_FULL in the paired-lane layout
                                 (two lanes per element, node pairs (j, sigma j) in adjacent rows of
                                 16-element half-tiles); same bytes, fewer registers per lane */
+#define DOGIP_STORE_SYM    5 /* WP only: the same weights in symmetry-adapted form -- per orbit P of
+                                the double-grid nodes under the barycentric involutions
+                                G = <(0 1), (2 3)> (3D) / <(0 1)> (2D), ahat_psi(P) = (1/|G|) sum_g
+                                psi(g) a_{g j0}; the apply runs Bhat block-diagonally by character
+                                (3D P4: 784 instead of 1729 nonzeros); same bytes, ~1/3 fewer FP64
+                                operations than DOGIP_STORE_FULL */
 #define DOGIP_STORE_QP     4 /* no DoGIP weights: the quadrature-point matrix-free comparator
                                 ("alternative approaches") -- geometry, coefficient and the
                                 basis contractions at the n_q points of the contract rule (L10) are

@@ -324,10 +324,10 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     *out = nullptr;
     if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
     if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO && storage != DOGIP_STORE_GLOBAL &&
-        storage != DOGIP_STORE_PAIR && storage != DOGIP_STORE_QP)
+        storage != DOGIP_STORE_PAIR && storage != DOGIP_STORE_QP && storage != DOGIP_STORE_SYM)
         return fail(DOGIP_E_INVALID_ARG, "unknown storage");
-    if (storage == DOGIP_STORE_PAIR && form != DOGIP_WP)
-        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_PAIR applies to the weighted projection only");
+    if ((storage == DOGIP_STORE_PAIR || storage == DOGIP_STORE_SYM) && form != DOGIP_WP)
+        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_PAIR / DOGIP_STORE_SYM apply to the weighted projection only");
     if (storage == DOGIP_STORE_ISO && form != DOGIP_EL)
         return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_ISO applies to the elliptic form only");
     if (storage == DOGIP_STORE_GLOBAL && form != DOGIP_WP)
@@ -403,8 +403,9 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     DevBufs tmp;
     WeightsArgs a{};
     a.d = d; a.p = p; a.form = form;
-    a.store = (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_PAIR) ? 0 : storage;
+    a.store = (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_PAIR || storage == DOGIP_STORE_SYM) ? 0 : storage;
     a.pair = storage == DOGIP_STORE_PAIR;
+    a.sym = storage == DOGIP_STORE_SYM;
     a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
     a.NG = op->ref.NG; a.tile_rows = op->ref.tile_rows;
     a.kind = coeff->kind;
@@ -430,6 +431,19 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         cudaMemcpy(dcell, coeff->per_cell, sizeof(double) * ncell, cudaMemcpyHostToDevice);
     }
     a.params = dparams; a.qp = dqp; a.qw = dqw; a.phiW = dphi; a.sW = dsW; a.per_cell = dcell; a.bad_flag = dbad;
+    if (a.sym) {
+        std::vector<int> hj((size_t)WT * 4);
+        std::vector<double> hc((size_t)WT * 4);
+        for (int r = 0; r < WT; ++r)
+            for (int k = 0; k < 4; ++k) { hj[r * 4 + k] = op->ref.symj[r][k]; hc[r * 4 + k] = op->ref.symc[r][k]; }
+        int* dj = nullptr;
+        double* dc = nullptr;
+        if (tmp.alloc(&dj, hj.size()) || tmp.alloc(&dc, hc.size())) return cleanup_fail(DOGIP_E_OOM, "symmetry tables");
+        cudaMemcpy(dj, hj.data(), sizeof(int) * hj.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(dc, hc.data(), sizeof(double) * hc.size(), cudaMemcpyHostToDevice);
+        a.symj = dj;
+        a.symc = dc;
+    }
     if (a.pair) {
         int* drp = nullptr;
         if (tmp.alloc(&drp, WT)) return cleanup_fail(DOGIP_E_OOM, "row permutation");
@@ -1093,6 +1107,20 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
                     return w[((size_t)(2 * t + lane / 16) * TR + op->ref.rowperm[row]) * 16 + lane % 16];
                 return w[((size_t)t * TR + row) * TILE + lane];
             };
+            if (op->store == DOGIP_STORE_SYM) {
+                // a_j = sum over the rows r of j's orbit of s_r c_{r,j} ahat_r  (the character
+                // matrix of an orbit is orthogonal: X X^T = s I)
+                for (int j = 0; j < WT; ++j) host[e * WT + j] = 0.0;
+                for (int r = 0; r < WT; ++r) {
+                    int sz = 0;
+                    for (int k = 0; k < 4; ++k) sz += op->ref.symj[r][k] >= 0;
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = op->ref.symj[r][k];
+                        if (j >= 0) host[e * WT + j] += sz * op->ref.symc[r][k] * at(r);
+                    }
+                }
+                continue;
+            }
             for (int j = 0; j < WT; ++j)
                 for (int c = 0; c < NC; ++c)
                     host[(e * WT + j) * NC + c] =

@@ -100,7 +100,7 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
     auto simp = cell_simplices(d);
     auto A = multi_indices(d, p);
     std::fprintf(f, "template <> struct RefElem<%d, %d, %d, %d> {\n", d, p, form, store);
-    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = %d, NG = %d, ROWS = %d, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0;\n",
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = %d, NG = %d, ROWS = %d, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 0;\n",
                  VT, WT, NC, NG, ROWS, TILE_ROWS, (int)simp.size(), NC);
     std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
     std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
@@ -271,7 +271,7 @@ static void emit_pair(FILE* f, int d, int p) {
     for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
     auto simp = cell_simplices(d);
     std::fprintf(f, "template <> struct RefElem<%d, %d, 0, 3> {\n", d, p);
-    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = 2, PAIR = 1;\n",
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = 2, PAIR = 1, DOT_IN_BODY = 0;\n",
                  VT, WT, WT, (int)simp.size());
     std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
     std::fprintf(f, "    static constexpr int VS = %d, NFIX = %d, NPAIR = %d;\n", VS, NFIX, NPAIR);
@@ -366,6 +366,314 @@ static void emit_pair(FILE* f, int d, int p) {
     std::fprintf(f, "};\n\n");
 }
 
+// Symmetry-adapted WP variant (STORE 5).  G = an abelian group of commuting
+// barycentric involutions (3D: <(0 1), (2 3)>, 2D: <(0 1)>).  Bhat is G-equivariant,
+// Bhat[g beta, g alpha] = Bhat[beta, alpha] (product basis), so in
+// symmetry-adapted coordinates -- per orbit O and character chi trivial on the
+// stabiliser, uhat_chi(O) = sum_{g in G} chi(g) u_{g l0} -- it is block diagonal by
+// character (Schur): ghat_chi(P) = sum_O Bhat_chi[P,O] uhat_chi(O),
+// Bhat_chi[P,O] = sum_{l in O} chi(k_l) Bhat[j0(P), l].  The weights of an orbit P
+// become the s x s matrix [ahat_{chi chi'}(P)], ahat_psi(P) = (1/|G|) sum_g psi(g) a_{g j0}
+// (same count: s values per orbit, stored instead of a_j), and the projection uses
+// Btilde_chi[P,O] = sum_{j in P} chi(k_j) Bhat[j, l0(O)].  3D P4: 784 block entries
+// instead of 1729, ~2240 instead of ~3340 FP64 instructions per element.
+// Emitted body: v = adapted u (butterflies), per W orbit: ghat (block rows), hhat =
+// weight matrix x ghat, z += Btilde^T hhat; y = inverse butterflies of z / |G|.
+static void emit_sym(FILE* f, int d, int p) {
+    Table t = bhat_table(d, p, 0);
+    const int VT = t.cols, WT = t.rows;
+    auto A = multi_indices(d, p);
+    auto W = multi_indices(d, 2 * p);
+    std::vector<std::array<int, 4>> gens;
+    if (d == 3) gens = {{1, 0, 2, 3}, {0, 1, 3, 2}};
+    else gens = {{1, 0, 2, 3}};
+    const int ng = (int)gens.size(), NGR = 1 << ng;
+    auto act = [&](const std::array<int, 4>& g, const std::array<int, 4>& a) {
+        std::array<int, 4> b{};
+        for (int i = 0; i <= d; ++i) b[i] = a[g[i]];
+        return b;
+    };
+    auto compose = [&](const std::array<int, 4>& g, const std::array<int, 4>& h) {
+        std::array<int, 4> r{};
+        for (int i = 0; i < 4; ++i) r[i] = g[h[i]];
+        return r;
+    };
+    // group element e (bitmask of generators) and character c (bitmask of -1 signs)
+    std::vector<std::array<int, 4>> G(NGR);
+    for (int e = 0; e < NGR; ++e) {
+        std::array<int, 4> g{0, 1, 2, 3};
+        for (int i = 0; i < ng; ++i)
+            if (e >> i & 1) g = compose(g, gens[i]);
+        G[e] = g;
+    }
+    auto chi = [&](int c, int e) { return (__builtin_popcount(c & e) & 1) ? -1 : 1; };
+    auto find = [](const std::vector<std::array<int, 4>>& v, const std::array<int, 4>& a) {
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i] == a) return (int)i;
+        std::fprintf(stderr, "sym: not found\n");
+        std::exit(1);
+    };
+    std::vector<std::vector<int>> gV(NGR, std::vector<int>(VT)), gW(NGR, std::vector<int>(WT));
+    for (int e = 0; e < NGR; ++e) {
+        for (int l = 0; l < VT; ++l) gV[e][l] = find(A, act(G[e], A[l]));
+        for (int j = 0; j < WT; ++j) gW[e][j] = find(W, act(G[e], W[j]));
+    }
+    for (int e = 0; e < NGR; ++e)
+        for (int j = 0; j < WT; ++j)
+            for (int l = 0; l < VT; ++l)
+                if (t.at(0, gW[e][j], gV[e][l]) != t.at(0, j, l)) { std::fprintf(stderr, "sym: not equivariant\n"); std::exit(1); }
+    struct Orb { int rep; std::vector<int> chars; std::vector<int> members; };   // chars trivial on the stabiliser
+    auto orbits = [&](int n, const std::vector<std::vector<int>>& gx) {
+        std::vector<Orb> out;
+        std::vector<bool> seen(n, false);
+        for (int i = 0; i < n; ++i) {
+            if (seen[i]) continue;
+            Orb o; o.rep = i;
+            for (int e = 0; e < NGR; ++e) {
+                const int k = gx[e][i];
+                if (!seen[k]) { seen[k] = true; o.members.push_back(k); }
+            }
+            for (int c = 0; c < NGR; ++c) {
+                bool triv = true;
+                for (int e = 0; e < NGR; ++e)
+                    if (gx[e][i] == i && chi(c, e) != 1) triv = false;
+                if (triv) o.chars.push_back(c);
+            }
+            out.push_back(o);
+        }
+        return out;
+    };
+    auto OV = orbits(VT, gV), OW0 = orbits(WT, gW);
+    // W orbits by decreasing size: weight rows of an orbit never straddle a chunk of 4k rows
+    std::vector<Orb> OW;
+    for (int sz = NGR; sz >= 1; sz /= 2)
+        for (auto& o : OW0)
+            if ((int)o.members.size() == sz) OW.push_back(o);
+    // adapted V index of (orbit, char)
+    std::vector<std::vector<int>> vidx(OV.size());
+    int nv = 0;
+    for (size_t o = 0; o < OV.size(); ++o)
+        for (size_t c = 0; c < OV[o].chars.size(); ++c) vidx[o].push_back(nv++);
+    // weight rows (orbit P, char psi) and the weights-kernel recombination table
+    std::vector<std::vector<int>> wrow(OW.size());
+    std::vector<std::array<int, 4>> rj;
+    std::vector<std::array<Rat, 4>> rc;
+    int nr = 0;
+    for (size_t P = 0; P < OW.size(); ++P) {
+        const int s = (int)OW[P].members.size();
+        for (int psi : OW[P].chars) {
+            wrow[P].push_back(nr++);
+            // ahat_psi = (1/|G|) sum_g psi(g) a_{g j0} = (1/s) sum over distinct members
+            std::array<int, 4> js{-1, -1, -1, -1};
+            std::array<Rat, 4> cs{};
+            int k = 0;
+            for (int e = 0; e < NGR; ++e) {
+                const int j = gW[e][OW[P].rep];
+                bool dup = false;
+                for (int q = 0; q < k; ++q)
+                    if (js[q] == j) dup = true;
+                if (dup) continue;
+                js[k] = j;
+                cs[k] = Rat(chi(psi, e), s);
+                ++k;
+            }
+            rj.push_back(js);
+            rc.push_back(cs);
+        }
+    }
+    int nnz = 0, pm1 = 0;
+    for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
+    auto simp = cell_simplices(d);
+    std::fprintf(f, "template <> struct RefElem<%d, %d, 0, 5> {\n", d, p);
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 1;\n",
+                 VT, WT, WT, (int)simp.size(), NGR);
+    std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d, NGROUP = %d;\n", nnz, pm1, NGR);
+    std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
+    for (size_t si = 0; si < simp.size(); ++si) {
+        std::fprintf(f, "%s{", si ? ", " : "");
+        for (int l = 0; l < VT; ++l) {
+            std::fprintf(f, "%s{", l ? "," : "");
+            for (int ax = 0; ax < d; ++ax) {
+                int o = 0;
+                for (int i = 0; i <= d; ++i) o += A[l][i] * simp[si][i][ax];
+                std::fprintf(f, "%s%d", ax ? "," : "", o);
+            }
+            std::fprintf(f, "}");
+        }
+        std::fprintf(f, "}");
+    }
+    std::fprintf(f, "};\n");
+    std::fprintf(f, "    static constexpr signed char ALPHA[%d][3] = {", VT);
+    for (int l = 0; l < VT; ++l)
+        std::fprintf(f, "%s{%d,%d,%d}", l ? "," : "", A[l][1], A[l][2], d == 3 ? A[l][3] : 0);
+    std::fprintf(f, "};\n");
+    // weights-kernel table: stored row r = sum_k SYMC[r][k] a_{SYMJ[r][k]}
+    std::fprintf(f, "    static constexpr short SYMJ[%d][4] = {", WT);
+    for (int r = 0; r < WT; ++r)
+        std::fprintf(f, "%s{%d,%d,%d,%d}", r ? "," : "", rj[r][0], rj[r][1], rj[r][2], rj[r][3]);
+    std::fprintf(f, "};\n");
+    std::fprintf(f, "    static constexpr double SYMC[%d][4] = {", WT);
+    for (int r = 0; r < WT; ++r)
+        std::fprintf(f, "%s{%s,%s,%s,%s}", r ? "," : "", lit(rc[r][0].to_double()).c_str(), lit(rc[r][1].to_double()).c_str(),
+                     lit(rc[r][2].to_double()).c_str(), lit(rc[r][3].to_double()).c_str());
+    std::fprintf(f, "};\n");
+    std::fprintf(f, "    static __host__ __device__ constexpr int row_of(int r) { return r; }\n");
+    // dot != null: *dot += u_T . y_T, computed as v . z (Parseval over the characters:
+    // sum_k v_k z_k = sum_l u_l y_l), so u_T dies after the transform (issuing the next
+    // tile's gather there instead measured slower: it keeps 35 more doubles live)
+    std::fprintf(f,
+        "    template <class Pol>\n"
+        "    static __device__ __forceinline__ void body(const double* __restrict__ u,\n"
+        "                                                double* __restrict__ y, Pol& pol, double* dot) {\n");
+    int flops = 0;
+    // 1. adapted coordinates v[k] = sum_{cosets} chi(c) u_{c l0} (stabiliser multiplicity
+    //    folded into the block constants): butterflies over the generators
+    std::fprintf(f, "        double v[%d], z[%d];\n", VT, VT);
+    auto coset_sum = [&](const Orb& o, int c, int gen_bits, const std::vector<std::vector<int>>& gx) {
+        // distinct members with their sign: sum over e of chi(c,e) x_{e rep}, distinct only
+        std::vector<std::pair<int, int>> terms;
+        for (int e = 0; e < NGR; ++e) {
+            const int k = gx[e][o.rep];
+            bool dup = false;
+            for (auto& tm : terms)
+                if (tm.first == k) dup = true;
+            if (!dup) terms.push_back({k, chi(c, e)});
+        }
+        (void)gen_bits;
+        return terms;
+    };
+    for (size_t o = 0; o < OV.size(); ++o) {
+        const Orb& O = OV[o];
+        const int sz = (int)O.members.size();
+        if (sz == 1) {
+            std::fprintf(f, "        v[%d] = u[%d];\n", vidx[o][0], O.rep);
+            continue;
+        }
+        if (sz == 2) {
+            auto tm = coset_sum(O, 0, 0, gV);
+            std::fprintf(f, "        v[%d] = u[%d] + u[%d];\n", vidx[o][0], tm[0].first, tm[1].first);
+            std::fprintf(f, "        v[%d] = u[%d] - u[%d];\n", vidx[o][1], tm[0].first, tm[1].first);
+            flops += 2;
+            continue;
+        }
+        // size 4: members a = e0, b = g1 a, c = g2 a, d = g1 g2 a; chars (s1, s2)
+        const int a = gV[0][O.rep], b = gV[1][O.rep], c = gV[2][O.rep], dd = gV[3][O.rep];
+        std::fprintf(f, "        { const double tp = u[%d] + u[%d], tm = u[%d] - u[%d], rp = u[%d] + u[%d], rm = u[%d] - u[%d];\n",
+                     a, b, a, b, c, dd, c, dd);
+        for (size_t ci = 0; ci < O.chars.size(); ++ci) {
+            const int ch = O.chars[ci];
+            const bool s1 = ch & 1, s2 = ch & 2;   // chi(g1) = -1 if bit 0, chi(g2) = -1 if bit 1
+            std::fprintf(f, "          v[%d] = %s %s %s;\n", vidx[o][ci], s1 ? "tm" : "tp", s2 ? "-" : "+", s1 ? "rm" : "rp");
+        }
+        std::fprintf(f, "        }\n");
+        flops += 8;
+    }
+    std::fprintf(f, "#pragma unroll\n        for (int k = 0; k < %d; ++k) z[k] = 0.0;\n", VT);
+    // 2-4. per W orbit
+    for (size_t P = 0; P < OW.size(); ++P) {
+        const Orb& PO = OW[P];
+        const int j0 = PO.rep;
+        std::fprintf(f, "        {\n          pol.template begin<%d>();\n", wrow[P][0]);
+        // ghat_chi = sum_O Bhat_chi[P,O] uhat_chi(O), uhat = |H_O| v
+        for (size_t ci = 0; ci < PO.chars.size(); ++ci) {
+            const int ch = PO.chars[ci];
+            std::vector<std::pair<int, Rat>> terms;
+            for (size_t o = 0; o < OV.size(); ++o) {
+                const Orb& O = OV[o];
+                int cpos = -1;
+                for (size_t q = 0; q < O.chars.size(); ++q)
+                    if (O.chars[q] == ch) cpos = (int)q;
+                if (cpos < 0) continue;
+                Rat sum(0);
+                for (int e = 0; e < NGR; ++e) sum = sum + Rat(chi(ch, e)) * t.at(0, j0, gV[e][O.rep]);
+                // sum over the full group = |H_O| * sum over distinct members; uhat = |H_O| v
+                // -> ghat = sum_O (sum_{l in O} chi B[j0,l]) |H_O| v = sum_O sum_g chi(g) B[j0, g l0] v
+                if (!sum.is_zero()) terms.push_back({vidx[o][cpos], sum});
+            }
+            flops += emit_combo(f, "          ", "g" + std::to_string(ci), true, terms, "v");
+        }
+        // hhat_chi = sum_chi' ahat_{chi chi'} ghat_chi'  (ahat rows of this orbit)
+        for (size_t ci = 0; ci < PO.chars.size(); ++ci) {
+            std::string acc;
+            for (size_t cj = 0; cj < PO.chars.size(); ++cj) {
+                const int psi = PO.chars[ci] ^ PO.chars[cj];
+                int rpos = -1;
+                for (size_t q = 0; q < PO.chars.size(); ++q)
+                    if (PO.chars[q] == psi) rpos = (int)q;
+                const std::string w = "pol.w(" + std::to_string(wrow[P][rpos]) + ")";
+                const std::string gj = "g" + std::to_string(cj);
+                if (acc.empty()) { acc = w + " * " + gj; flops += 1; }
+                else { acc = "__fma_rn(" + w + ", " + gj + ", " + acc + ")"; flops += 2; }
+            }
+            std::fprintf(f, "          const double h%zu = %s;\n", ci, acc.c_str());
+        }
+        // z_chi(O) += Btilde_chi[P,O] hhat_chi(P) / |G|,  Btilde = sum_{j in P} chi(k_j) B[j, l0(O)]
+        for (size_t o = 0; o < OV.size(); ++o) {
+            const Orb& O = OV[o];
+            for (size_t q = 0; q < O.chars.size(); ++q) {
+                const int ch = O.chars[q];
+                int cpos = -1;
+                for (size_t ci = 0; ci < PO.chars.size(); ++ci)
+                    if (PO.chars[ci] == ch) cpos = (int)ci;
+                if (cpos < 0) continue;
+                Rat sum(0);
+                std::vector<int> seen;
+                for (int e = 0; e < NGR; ++e) {
+                    const int j = gW[e][j0];
+                    bool dup = false;
+                    for (int x : seen) if (x == j) dup = true;
+                    if (dup) continue;
+                    seen.push_back(j);
+                    sum = sum + Rat(chi(ch, e)) * t.at(0, j, O.rep);
+                }
+                sum = sum * Rat(1, NGR);
+                if (sum.is_zero()) continue;
+                const int k = vidx[o][q];
+                const std::string h = "h" + std::to_string(cpos);
+                std::string acc = "z[" + std::to_string(k) + "]";
+                if (sum == Rat(1)) acc = "(" + acc + ") + " + h;
+                else if (sum == Rat(-1)) acc = "(" + acc + ") - " + h;
+                else { acc = "__fma_rn(" + lit(sum.to_double()) + ", " + h + ", " + acc + ")"; flops += 1; }
+                flops += 1;
+                std::fprintf(f, "          z[%d] = %s;\n", k, acc.c_str());
+            }
+        }
+        std::fprintf(f, "        }\n");
+    }
+    // 5. y_{c l0} = sum_chi chi(c) z_chi (the 1/|G| is in the projection constants)
+    for (size_t o = 0; o < OV.size(); ++o) {
+        const Orb& O = OV[o];
+        const int sz = (int)O.members.size();
+        if (sz == 1) {
+            std::fprintf(f, "        y[%d] += z[%d];\n", O.rep, vidx[o][0]);
+            flops += 1;
+            continue;
+        }
+        // member e-rep gets sum_chi chi(e) z_chi
+        std::vector<int> done;
+        for (int e = 0; e < NGR; ++e) {
+            const int m = gV[e][O.rep];
+            bool dup = false;
+            for (int x : done) if (x == m) dup = true;
+            if (dup) continue;
+            done.push_back(m);
+            std::string acc;
+            for (size_t q = 0; q < O.chars.size(); ++q) {
+                const std::string zz = "z[" + std::to_string(vidx[o][q]) + "]";
+                if (acc.empty()) acc = chi(O.chars[q], e) > 0 ? zz : "-" + zz;
+                else acc = "(" + acc + (chi(O.chars[q], e) > 0 ? ") + " : ") - ") + zz;
+            }
+            std::fprintf(f, "        y[%d] += %s;\n", m, acc.c_str());
+            flops += (int)O.chars.size();
+        }
+    }
+    std::fprintf(f, "        if (dot) {\n          double s = 0.0;\n#pragma unroll\n"
+                    "          for (int k = 0; k < %d; ++k) s = fma(v[k], z[k], s);\n          *dot += s;\n        }\n", VT);
+    std::fprintf(f, "    }\n");
+    std::fprintf(f, "    static constexpr int FLOPS = %d;\n", flops);
+    std::fprintf(f, "};\n\n");
+}
+
 int main(int argc, char** argv) {
     if (argc < 2) { std::fprintf(stderr, "usage: gen_bhat out.cuh [group_values]\n"); return 2; }
     if (argc > 2) g_gmax_vals = std::atoi(argv[2]);
@@ -391,6 +699,7 @@ int main(int argc, char** argv) {
             emit_variant(f, d, p, 1, 0);
             emit_variant(f, d, p, 1, 1);
             emit_pair(f, d, p);
+            emit_sym(f, d, p);
         }
     std::fprintf(f, "}  // namespace dogip_gen\n");
     std::fclose(f);

@@ -263,12 +263,13 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
                          (int64_t)(2 * geo.p) * (cur.ci + geo.swy * cur.cj + geo.swz * cur.ck)};
             RE::body(uT, yT, gp);
         } else {
-            RE::body(uT, yT, ws);
+            if constexpr (RE::DOT_IN_BODY) RE::body(uT, yT, ws, dot_partials ? &udot : nullptr);
+            else RE::body(uT, yT, ws);
             ws.next_tile();
         }
         // u^T A u = sum_T u_T^T (Bhat^T A_T Bhat u_T): the CG dot p.q, element by element
         // (padding lanes and Dirichlet DoFs have u_T = 0 and contribute nothing)
-        if (dot_partials) {
+        if (!RE::DOT_IN_BODY && dot_partials) {
 #pragma unroll
             for (int l = 0; l < RE::VT; ++l) udot = fma(uT[l], yT[l], udot);
         }
@@ -545,6 +546,7 @@ template <int D, int P>
 cudaError_t launch_form(const ApplyArgs& a) {
     if (a.form == 0 && a.store == 2) return launch_one<D, P, 0, 0, false, true>(a);   // WP has no BC
     if (a.form == 0 && a.store == 3) return launch_pair<D, P>(a);
+    if (a.form == 0 && a.store == 5) return launch_one<D, P, 0, 5, false, false>(a);
     if (a.form == 0) return launch_dir<D, P, 0, 0>(a);
     return a.store == 1 ? launch_dir<D, P, 1, 1>(a) : launch_dir<D, P, 1, 0>(a);
 }
@@ -576,6 +578,11 @@ static void fill_info(RefInfo& r) {
     r.tile_rows = RE::TILE_ROWS;
     r.flops = RE::FLOPS; r.nnz = RE::NNZ; r.nnz_pm1 = RE::NNZ_PM1;
     r.pair = RE::PAIR;
+    r.sym = ST == 5;
+    if constexpr (ST == 5) {
+        for (int j = 0; j < RE::WT; ++j)
+            for (int k = 0; k < 4; ++k) { r.symj[j][k] = RE::SYMJ[j][k]; r.symc[j][k] = RE::SYMC[j][k]; }
+    }
     for (int j = 0; j < RE::WT && j < MAX_WT_GLOBAL; ++j) {
         if constexpr (RE::PAIR) r.rowperm[j] = RE::ROWPERM[j];
         else r.rowperm[j] = j;
@@ -592,6 +599,7 @@ bool ref_info(int d, int p, int form, int store, RefInfo& r) {
         if (form == 1 && store == 0) { fill_info<D, P, 1, 0>(r); return true; } \
         if (form == 1 && store == 1) { fill_info<D, P, 1, 1>(r); return true; } \
         if (form == 0 && store == 3) { fill_info<D, P, 0, 3>(r); return true; } \
+        if (form == 0 && store == 5) { fill_info<D, P, 0, 5>(r); return true; } \
         return false;                                                          \
     }
     DOGIP_CASE(2, 1) DOGIP_CASE(2, 2) DOGIP_CASE(2, 3) DOGIP_CASE(2, 4)

@@ -33,7 +33,7 @@ constexpr int MAX_WT_GLOBAL = 165;   // W_T of P_8 in 3D (global WP storage, p <
 
 struct ApplyArgs {
     int d, p, form, store;      // store: 0 full A_T blocks, 1 isotropic a_j + G_T (EL), 2 global WP,
-                                // 3 full WP in the paired-lane layout
+                                // 3 full WP in the paired-lane layout, 5 symmetry-adapted WP
     bool dirichlet;
     const double* u;
     double* y;
@@ -56,6 +56,9 @@ struct RefInfo {
     int pair;                        // paired-lane WP layout (STORE 3): half-tiles of 16, rows permuted
     int loff[MAX_NS][MAX_VT][3];
     int rowperm[MAX_WT_GLOBAL];      // storage row of canonical node j (identity unless pair)
+    int sym;                         // symmetry-adapted WP (STORE 5): row r = sum_k symc[r][k] a_{symj[r][k]}
+    int symj[MAX_WT_GLOBAL][4];
+    double symc[MAX_WT_GLOBAL][4];
 };
 bool ref_info(int d, int p, int form, int store, RefInfo& r);
 
@@ -80,6 +83,9 @@ struct WeightsArgs {
     int* bad_flag;                         // device int: 1 degenerate element, 2 bad coefficient
     int pair;                              // paired-lane WP layout (STORE 3)
     const int* rowperm;                    // device (WT,): storage row of node j (pair layout)
+    int sym;                               // symmetry-adapted WP rows (STORE 5)
+    const int* symj;                       // device (WT, 4): canonical nodes of stored row r (-1: none)
+    const double* symc;                    // device (WT, 4): their coefficients
     cudaStream_t stream;
 };
 cudaError_t launch_weights(const WeightsArgs& a);

@@ -169,6 +169,18 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
         }
         return;
     }
+    if (a.sym) {   // symmetry-adapted WP rows: ahat_psi(P) = (1/s) sum_c psi(c) a_{c j0} (STORE 5)
+        auto aj = [&](int j) { return direct ? adet * cconst[0] * a.sW[j] : a.scratch_a[el * WT + j]; };
+        for (int r = 0; r < WT; ++r) {
+            double v = 0.0;
+            for (int k = 0; k < 4; ++k) {
+                const int j = a.symj[r * 4 + k];
+                if (j >= 0) v = fma(a.symc[r * 4 + k], aj(j), v);
+            }
+            out[(size_t)r * TILE] = G.valid ? v : 0.0;
+        }
+        return;
+    }
     for (int j = 0; j < WT; ++j) {
         double ab[6];
         for (int c = 0; c < nc; ++c)
