@@ -32,6 +32,9 @@
 #include "apply.cuh"
 #include "common.cuh"
 
+#ifndef DOGIP_SYM_UPF
+#define DOGIP_SYM_UPF 1        // symmetry-adapted body: stage the next tile's u_T in shared memory
+#endif
 #ifndef DOGIP_STAGES
 #define DOGIP_STAGES 4          // ring stages per warp
 #endif
@@ -67,7 +70,9 @@ struct Chunking {
     static constexpr int S = DOGIP_STAGES;
     static constexpr int TILE_ROWS = RE::TILE_ROWS;
     static constexpr int AL = RE::RALIGN;                                  // chunk boundaries fall on rows % AL == 0
-    static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA : DOGIP_ROWS_2CTA;
+    // the symmetry-adapted kernel stages u_T in shared memory too: 16-row chunks keep 2 CTAs/SM
+    static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA
+                                     : (DOGIP_SYM_UPF && RE::DOT_IN_BODY) ? 16 : DOGIP_ROWS_2CTA;
     static constexpr int ROWS_MAX = (ROWS_MAX0 / AL) * AL;
     static constexpr int NCH0 = (TILE_ROWS + ROWS_MAX - 1) / ROWS_MAX;
     static constexpr int ROWS_B = (TILE_ROWS + NCH0 - 1) / NCH0;
@@ -203,6 +208,15 @@ __device__ __forceinline__ void gather(const double* __restrict__ u, const ElemC
     }
 }
 
+// u_T of a tile -> the warp's [VT][32] shared buffer with cp.async (no registers held)
+template <class RE, int L = 0>
+__device__ __forceinline__ void gather_async(const double* __restrict__ u, const ElemCtx& c, uint32_t ubuf_lane) {
+    if constexpr (L < RE::VT) {
+        if (c.valid && !((c.skip >> L) & 1ull)) cp_async8(ubuf_lane + 8u * TILE * L, u + c.base + dof_off<RE, L>(c));
+        gather_async<RE, L + 1>(u, c, ubuf_lane);
+    }
+}
+
 template <class RE, int L = 0>
 __device__ __forceinline__ void scatter(double* __restrict__ y, const ElemCtx& c, const double* yT) {
     if constexpr (L < RE::VT) {
@@ -222,6 +236,8 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* rings = reinterpret_cast<double*>(smem_raw);
     uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)NW * C::S * C::ROWS * TILE);
+    constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
+    double* ubufs = reinterpret_cast<double*>(bars + NW * C::S);            // [NW][VT][32] (UPF only)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw = tile_begin + (int64_t)blockIdx.x * NW + warp;
@@ -250,6 +266,35 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     double udot = 0.0;
     double uT[RE::VT];
     ElemCtx cur{};
+    if constexpr (UPF) {
+        double* ubuf = ubufs + (size_t)warp * RE::VT * TILE;
+        const uint32_t ubuf_lane = smem_u32(ubuf + lane);
+        if (gw < tile_end) {
+            cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
+            gather_async<RE>(u, cur, ubuf_lane);
+        }
+        cp_async_commit();
+        for (int64_t tile = gw; tile < tile_end; tile += nw) {
+            cp_async_wait_all();
+            __syncwarp();
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l)
+                uT[l] = (cur.valid && !((cur.skip >> l) & 1ull)) ? ubuf[l * TILE + lane] : 0.0;
+            __syncwarp();
+            const ElemCtx prev = cur;
+            if (tile + nw < tile_end) {         // next tile's u_T lands in smem during this body
+                cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
+                gather_async<RE>(u, cur, ubuf_lane);
+            }
+            cp_async_commit();
+            double yT[RE::VT];
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
+            if constexpr (RE::DOT_IN_BODY) RE::body(uT, yT, ws, dot_partials ? &udot : nullptr);
+            ws.next_tile();
+            if (prev.valid) scatter<RE>(y, prev, yT);
+        }
+    } else {
     if (gw < tile_end) {
         cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
         gather<RE>(u, cur, uT);
@@ -279,6 +324,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
             gather<RE>(u, cur, uT);
         }
         if (prev.valid) scatter<RE>(y, prev, yT);
+    }
     }
     if (dot_partials) {     // deterministic: one partial per warp, fixed order reduction later
         for (int o = 16; o > 0; o >>= 1) udot += __shfl_xor_sync(0xffffffffu, udot, o);
@@ -508,7 +554,9 @@ cudaError_t launch_one(const ApplyArgs& a) {
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
-    const size_t smem = GLOB ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8;
+    constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
+    const size_t smem = GLOB ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8 +
+                                   (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0);
     auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
     static int configured = 0;   // per instantiation
     static int occ = 1;
