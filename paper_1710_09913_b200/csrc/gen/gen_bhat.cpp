@@ -574,6 +574,9 @@ static void emit_sym(FILE* f, int d, int p) {
         const Orb& PO = OW[P];
         const int j0 = PO.rep;
         std::fprintf(f, "        {\n          pol.template begin<%d>();\n", wrow[P][0]);
+        // the orbit's weights first: their shared-memory latency overlaps the block rows
+        for (size_t q = 0; q < PO.chars.size(); ++q)
+            std::fprintf(f, "          const double a%zu = pol.w(%d);\n", q, wrow[P][q]);
         // ghat_chi = sum_O Bhat_chi[P,O] uhat_chi(O), uhat = |H_O| v
         for (size_t ci = 0; ci < PO.chars.size(); ++ci) {
             const int ch = PO.chars[ci];
@@ -600,7 +603,7 @@ static void emit_sym(FILE* f, int d, int p) {
                 int rpos = -1;
                 for (size_t q = 0; q < PO.chars.size(); ++q)
                     if (PO.chars[q] == psi) rpos = (int)q;
-                const std::string w = "pol.w(" + std::to_string(wrow[P][rpos]) + ")";
+                const std::string w = "a" + std::to_string(rpos);
                 const std::string gj = "g" + std::to_string(cj);
                 if (acc.empty()) { acc = w + " * " + gj; flops += 1; }
                 else { acc = "__fma_rn(" + w + ", " + gj + ", " + acc + ")"; flops += 2; }

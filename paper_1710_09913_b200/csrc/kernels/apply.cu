@@ -65,14 +65,30 @@ constexpr int min_blocks() {
 // Balanced chunks of whole nodes: NCH = ceil(TILE_ROWS / ROWS_MAX) chunks of ROWS rows
 // (a multiple of NC, so a node's NC rows never straddle two chunks; the NG leading
 // rows of the iso storage sit in chunk 0), the last chunk shorter.
+#ifndef DOGIP_SYM_ROWS
+#define DOGIP_SYM_ROWS 24      // rows per chunk of the symmetry-adapted kernel (u_T staging shares smem)
+#endif
+#ifndef DOGIP_SYM_STAGES
+#define DOGIP_SYM_STAGES 2
+#endif
+#ifndef DOGIP_STAGES_FORCE
+#define DOGIP_STAGES_FORCE 0   // > 0: every kernel uses this many stages (A/B builds)
+#endif
 template <class RE, int TW = TILE>
 struct Chunking {
-    static constexpr int S = DOGIP_STAGES;
+    // ring stages per (d, p, form, storage), from the B200 A/B of 2/3/4 stages
+    // (profiles/r01_ab_ring_stages.log): double buffering wins for the long weight tiles of
+    // 3D P3 EL (C4: 3.72 -> 3.45 ms), 2D P4 EL and the symmetry-adapted kernel, 4 stages
+    // for the rest (C2 p=2, C3, C4 iso, C5 full lose 1-6 % with 2)
+    static constexpr int S = DOGIP_STAGES_FORCE > 0 ? DOGIP_STAGES_FORCE
+                           : RE::DOT_IN_BODY ? DOGIP_SYM_STAGES
+                           : (RE::NC > 1 && RE::TILE_ROWS >= 84) ? 2
+                           : DOGIP_STAGES;
     static constexpr int TILE_ROWS = RE::TILE_ROWS;
     static constexpr int AL = RE::RALIGN;                                  // chunk boundaries fall on rows % AL == 0
     // the symmetry-adapted kernel stages u_T in shared memory too: 16-row chunks keep 2 CTAs/SM
     static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA
-                                     : (DOGIP_SYM_UPF && RE::DOT_IN_BODY) ? 16 : DOGIP_ROWS_2CTA;
+                                     : (DOGIP_SYM_UPF && RE::DOT_IN_BODY) ? DOGIP_SYM_ROWS : DOGIP_ROWS_2CTA;
     static constexpr int ROWS_MAX = (ROWS_MAX0 / AL) * AL;
     static constexpr int NCH0 = (TILE_ROWS + ROWS_MAX - 1) / ROWS_MAX;
     static constexpr int ROWS_B = (TILE_ROWS + NCH0 - 1) / NCH0;
