@@ -53,13 +53,19 @@ namespace {
 #ifndef DOGIP_MINB_LARGE
 #define DOGIP_MINB_LARGE 2   // CTAs/SM asked of ptxas when V_T > 20 (3D P4)
 #endif
+#ifndef DOGIP_MINB_SMALL
+#define DOGIP_MINB_SMALL 3   // CTAs/SM asked of ptxas when V_T <= 10 (2D P1-P3, 3D P1-P2)
+#endif
+#ifndef DOGIP_ROWS_4CTA
+#define DOGIP_ROWS_4CTA 12
+#endif
 #ifndef DOGIP_PAIR_MINB
 #define DOGIP_PAIR_MINB 4    // CTAs/SM of the paired-lane WP kernel (u_T, y_T halves: <= 128 registers)
 #endif
 template <class RE>
 constexpr int min_blocks() {
     if constexpr (RE::PAIR) return DOGIP_PAIR_MINB;   // paired-lane WP (STORE 3)
-    else return RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE;
+    else return RE::VT <= 10 ? DOGIP_MINB_SMALL : RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE;
 }
 
 // Balanced chunks of whole nodes: NCH = ceil(TILE_ROWS / ROWS_MAX) chunks of ROWS rows
@@ -87,7 +93,8 @@ struct Chunking {
     static constexpr int TILE_ROWS = RE::TILE_ROWS;
     static constexpr int AL = RE::RALIGN;                                  // chunk boundaries fall on rows % AL == 0
     // the symmetry-adapted kernel stages u_T in shared memory too: 16-row chunks keep 2 CTAs/SM
-    static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA
+    static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 4 ? DOGIP_ROWS_4CTA
+                                     : min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA
                                      : (DOGIP_SYM_UPF && RE::DOT_IN_BODY) ? DOGIP_SYM_ROWS : DOGIP_ROWS_2CTA;
     static constexpr int ROWS_MAX = (ROWS_MAX0 / AL) * AL;
     static constexpr int NCH0 = (TILE_ROWS + ROWS_MAX - 1) / ROWS_MAX;
