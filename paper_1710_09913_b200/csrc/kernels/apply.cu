@@ -165,6 +165,22 @@ struct WarpStream {
     }
 };
 
+#ifndef DOGIP_DIRECT_ROWS
+#define DOGIP_DIRECT_ROWS 6    // tiles with at most this many weight rows skip the smem ring
+#endif
+template <class RE>
+__host__ __device__ constexpr bool direct_weights() { return !RE::DOT_IN_BODY && !RE::PAIR && RE::TILE_ROWS <= DOGIP_DIRECT_ROWS; }
+
+// weights already in registers (direct-weights path): node rows are compile-time indices
+struct RegPol {
+    const double* wr;
+    template <int J>
+    __device__ __forceinline__ void begin() {}
+    template <int J>
+    __device__ __forceinline__ void end() {}
+    __device__ __forceinline__ double w(int k) const { return wr[k]; }
+};
+
 // Theorem 1 storage (global WP diagonal over W = C_{N,2p}): the weight of
 // double-grid node j of the element is gathered from the global W-lattice vector.
 struct GatherPol {
@@ -275,10 +291,12 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     ws.cons = 0;
     ws.policy = policy_evict_first();
     __shared__ int offw_s[GLOB ? MAX_NS * MAX_WT_GLOBAL : 1];
+    constexpr bool DW = direct_weights<RE>() && !GLOB;
     if constexpr (GLOB) {
         for (int i = threadIdx.x; i < MAX_NS * RE::WT; i += blockDim.x)
             offw_s[(i / RE::WT) * MAX_WT_GLOBAL + i % RE::WT] = offw_g[i];
         __syncthreads();
+    } else if (DW) {
     } else if (lane == 0) {
         for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
         fence_mbar_init();
@@ -289,7 +307,40 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     double udot = 0.0;
     double uT[RE::VT];
     ElemCtx cur{};
-    if constexpr (UPF) {
+    if constexpr (DW) {
+        // tiny tiles (<= DOGIP_DIRECT_ROWS weight rows): each lane reads its element's
+        // weights with coalesced read-only loads (one 256 B row per warp load), the next
+        // tile's together with its u_T gather -- no ring, barriers or bulk copies
+        double wr[RE::TILE_ROWS];
+        auto loadw = [&](int64_t t) {
+            const double* wt = w + t * C::TILE_DBL + lane;
+#pragma unroll
+            for (int k = 0; k < RE::TILE_ROWS; ++k) wr[k] = ldg_stream_f64(wt + k * TILE);
+        };
+        if (gw < tile_end) {
+            cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
+            gather<RE>(u, cur, uT);
+            loadw(gw);
+        }
+        for (int64_t tile = gw; tile < tile_end; tile += nw) {
+            double yT[RE::VT];
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
+            RegPol rp{wr};
+            RE::body(uT, yT, rp);
+            if (dot_partials) {
+#pragma unroll
+                for (int l = 0; l < RE::VT; ++l) udot = fma(uT[l], yT[l], udot);
+            }
+            const ElemCtx prev = cur;
+            if (tile + nw < tile_end) {
+                cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
+                gather<RE>(u, cur, uT);
+                loadw(tile + nw);
+            }
+            if (prev.valid) scatter<RE>(y, prev, yT);
+        }
+    } else if constexpr (UPF) {
         double* ubuf = ubufs + (size_t)warp * RE::VT * TILE;
         const uint32_t ubuf_lane = smem_u32(ubuf + lane);
         if (gw < tile_end) {
@@ -578,7 +629,8 @@ cudaError_t launch_one(const ApplyArgs& a) {
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
     constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
-    const size_t smem = GLOB ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8 +
+    constexpr bool DW = direct_weights<RE>() && !GLOB;
+    const size_t smem = (GLOB || DW) ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8 +
                                    (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0);
     auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
     static int configured = 0;   // per instantiation

@@ -100,6 +100,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 }
 
 __device__ __forceinline__ double ldg_f64(const double* p) { return __ldg(p); }
+// streamed read-only load, not kept in L1 (weights read exactly once)
+__device__ __forceinline__ double ldg_stream_f64(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
 
 // Ampere-style async copy global -> shared (LDGSTS), 8 bytes, L1-allocating
 __device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
