@@ -153,6 +153,17 @@ def oracle_sample_apply(cfg, n_cells: int, seed_offset: int = 0):
 _ORACLE_CACHE: dict = {}
 
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(cfg, target_s: float = 12.0) -> dict:
     """Oracle throughput in the metric's unit on a bounded element sample."""
     oracle_sample_apply(cfg, 8)                                     # warm caches / imports
@@ -162,7 +173,7 @@ def cpu_baseline(cfg, target_s: float = 12.0) -> dict:
     ne, t = oracle_sample_apply(cfg, n_cells, 1)
     frac = ne / cfg.n_elem
     gdofs = cfg.ndof * frac / t / 1e9
-    return {"value": gdofs, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": gdofs, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": _cpu_model(),
             "sample": f"oracle element route (NumPy, single-threaded einsum) over {ne} of {cfg.n_elem} "
                       f"elements ({n_cells} cells) of {cfg.name}; GDoF/s = ndof * sampled fraction / time",
             "seconds": t}

@@ -41,6 +41,49 @@ def time_apply(op, u, y, n, dirichlet):
     return e0.elapsed_time(e1) * 1e-3 / n
 
 
+_FLUSH = None
+
+
+def time_apply_flushed(op, u, y, n, dirichlet):
+    """Median per-apply time with the L2 (126 MB) flushed before every call by writing a
+    256 MB buffer -- the HBM number for inputs that would otherwise stay L2-resident."""
+    global _FLUSH
+    if _FLUSH is None:
+        _FLUSH = torch.empty(32 << 20, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream()
+    ts = []
+    for _ in range(n):
+        _FLUSH.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        op.apply(u, y, dirichlet=dirichlet)
+        e1.record(s)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3)
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def graph_latency(op, u, y, dirichlet, reps=200):
+    """Device latency of one apply replayed from a CUDA graph."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        op.apply(u, y, dirichlet=dirichlet, stream=s)       # configure before capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            op.apply(u, y, dirichlet=dirichlet, stream=s)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="C1,C2p1,C2p2,C2p3,C2p4,C3,C4,C5")
@@ -74,6 +117,8 @@ def main():
             dirichlet = form == 1
             n = args.iters if c.ndof > 1e6 else 200
             t_apply = time_apply(op, u, y, n, dirichlet)
+            t_flush = time_apply_flushed(op, u, y, 9, dirichlet) if c.ndof < 3e7 else None
+            t_graph = graph_latency(op, u, y, dirichlet) if c.ndof < 1e5 else None
             nw = oi["W_T"] + oi["n_c"] if storage == 1 else oi["W_T"] * oi["n_c"]
             alg = 8 * nw * c.n_elem + 16 * c.ndof
             if storage == 2:                      # global W vector read once (Theorem 1)
@@ -93,6 +138,10 @@ def main():
                    "apply_ms": t_apply * 1e3, "GDoF_s": c.ndof / t_apply / 1e9,
                    "alg_GB": alg / 1e9, "alg_GBs": alg / t_apply / 1e9, "frac_measured": alg / t_apply / 1e9 / PEAK,
                    "cg_ms_per_iter": r["seconds"] / n * 1e3, "cg_apply_ms": r["apply_seconds"] / n * 1e3}
+            if t_flush is not None:       # L2 flushed before each apply (median of 9)
+                row.update({"apply_ms_l2flushed": t_flush * 1e3, "frac_l2flushed": alg / t_flush / 1e9 / PEAK})
+            if t_graph is not None:
+                row["apply_graph_latency_us"] = t_graph * 1e6
             if args.solve and (name in ("C1", "C3", "C5")) and (name != "C1" or form == 1):
                 tol = 1e-12 if name == "C5" else 1e-10
                 x = torch.zeros_like(b)
