@@ -32,6 +32,10 @@
 #include "apply.cuh"
 #include "common.cuh"
 
+#ifndef DOGIP_LOCKSTEP
+#define DOGIP_LOCKSTEP -1      // CTA barrier at every weight chunk (the CTA's warps share I-cache
+                               // lines): -1 per-variant policy, 0 never, 1 always (A/B builds)
+#endif
 #ifndef DOGIP_SYM_UPF
 #define DOGIP_SYM_UPF 1        // symmetry-adapted body: stage the next tile's u_T in shared memory
 #endif
@@ -80,6 +84,15 @@ constexpr int min_blocks() {
 #ifndef DOGIP_STAGES_FORCE
 #define DOGIP_STAGES_FORCE 0   // > 0: every kernel uses this many stages (A/B builds)
 #endif
+// Lock-stepping the 4 warps of a CTA at every weight chunk (profiles/r01_ab_lockstep2.log):
+// -5 % for the FP64-bound ISO storage (C4 iso 2.47 -> 2.34 ms, C2 p=4 iso -14 %), -1 % for
+// the long full tiles of C4 / C5; +3 % for the symmetry-adapted kernel, +2 % for C2 p=4 EL
+template <class RE>
+__host__ __device__ constexpr bool lockstep() {
+    if constexpr (DOGIP_LOCKSTEP >= 0) return DOGIP_LOCKSTEP != 0;
+    else return !RE::DOT_IN_BODY && !RE::PAIR && (RE::NG > 0 || RE::TILE_ROWS >= 165);
+}
+
 template <class RE, int TW = TILE>
 struct Chunking {
     // ring stages per (d, p, form, storage), from the B200 A/B of 2/3/4 stages
@@ -145,6 +158,7 @@ struct WarpStream {
         constexpr int c_cur = RE::row_of(J) / C::ROWS;
         if constexpr (J == 0 || c_cur != RE::row_of(J - 1) / C::ROWS) {
             constexpr int gi = c_cur + C::S - 1;          // chunk refilled now, relative to this tile
+            if constexpr (lockstep<RE>()) asm volatile("bar.sync 1, %0;" ::"n"(APPLY_THREADS) : "memory");
             __syncwarp();
             if (lane == 0) {
                 fence_proxy_async_smem();                 // prior generic reads of the stage
@@ -180,6 +194,18 @@ struct RegPol {
     __device__ __forceinline__ void end() {}
     __device__ __forceinline__ double w(int k) const { return wr[k]; }
 };
+
+// LOCKSTEP: a warp with fewer tiles than its CTA's first warp matches the barriers the
+// others still execute (NCH per tile)
+template <class RE, class C>
+__device__ __forceinline__ void lockstep_tail(int64_t gw, int64_t tile_end, int64_t gw0, int64_t nw) {
+    if constexpr (lockstep<RE>()) {
+        const int64_t mine = gw < tile_end ? (tile_end - gw + nw - 1) / nw : 0;
+        const int64_t first = gw0 < tile_end ? (tile_end - gw0 + nw - 1) / nw : 0;
+        for (int64_t k = mine; k < first; ++k)
+            for (int c = 0; c < C::NCH; ++c) asm volatile("bar.sync 1, %0;" ::"n"(APPLY_THREADS) : "memory");
+    }
+}
 
 // Theorem 1 storage (global WP diagonal over W = C_{N,2p}): the weight of
 // double-grid node j of the element is gathered from the global W-lattice vector.
@@ -368,6 +394,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
             ws.next_tile();
             if (prev.valid) scatter<RE>(y, prev, yT);
         }
+        lockstep_tail<RE, C>(gw, tile_end, tile_begin + (int64_t)blockIdx.x * NW, nw);
     } else {
     if (gw < tile_end) {
         cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
@@ -399,6 +426,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
         }
         if (prev.valid) scatter<RE>(y, prev, yT);
     }
+    if constexpr (!GLOB) lockstep_tail<RE, C>(gw, tile_end, tile_begin + (int64_t)blockIdx.x * NW, nw);
     }
     if (dot_partials) {     // deterministic: one partial per warp, fixed order reduction later
         for (int o = 16; o > 0; o >>= 1) udot += __shfl_xor_sync(0xffffffffu, udot, o);
