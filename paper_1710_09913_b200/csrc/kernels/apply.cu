@@ -68,6 +68,9 @@ namespace {
 #endif
 template <class RE>
 constexpr int min_blocks() {
+#ifdef DOGIP_MINB_OVERRIDE
+    return DOGIP_MINB_OVERRIDE;
+#endif
     if constexpr (RE::PAIR) return DOGIP_PAIR_MINB;   // paired-lane WP (STORE 3)
     else return RE::VT <= 10 ? DOGIP_MINB_SMALL : RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE;
 }

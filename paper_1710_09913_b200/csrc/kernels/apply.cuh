@@ -13,7 +13,10 @@ namespace dogip {
 extern std::atomic<long long> g_launches;
 inline void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-constexpr int APPLY_THREADS = 128;   // 4 warps = 4 tiles in flight per CTA
+#ifndef DOGIP_APPLY_THREADS
+#define DOGIP_APPLY_THREADS 128
+#endif
+constexpr int APPLY_THREADS = DOGIP_APPLY_THREADS;   // 4 warps = 4 tiles in flight per CTA
 constexpr int APPLY_MAX_WARPS = 148 * 8 * 4;   // bound of the per-warp dot partials of one launch
 
 // Warp-uniform gather tables (kernel-parameter bank): off = local DoF index
