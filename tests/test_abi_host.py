@@ -132,3 +132,17 @@ def test_report_reproduces_paper_tables():
                 assert abs(r["comp_eff"] - g["comp_eff"]) <= 0.005 + 1e-12
             else:
                 assert r["mem_A"] >= g["mem_A"]
+
+
+def test_header_constants_match_binding():
+    """#define values of include/dogip.h (storage variants, flags, status codes) equal the
+    binding's constants -- the ABI cannot drift silently."""
+    text = open(HEADER).read()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(DOGIP_[A-Z0-9_]+)\s+(-?\d+)", text)}
+    for name in ("DOGIP_STORE_FULL", "DOGIP_STORE_ISO", "DOGIP_STORE_GLOBAL", "DOGIP_STORE_PAIR",
+                 "DOGIP_STORE_QP", "DOGIP_STORE_SYM", "DOGIP_DIRICHLET_ZERO", "DOGIP_NO_EXCHANGE",
+                 "DOGIP_CG_RESUME"):
+        assert name in defs, name
+        assert getattr(_lib, name) == defs[name], name
+    for code, label in _lib.STATUS.items():
+        assert defs.get("DOGIP_" + label) == code, label
