@@ -22,7 +22,8 @@ LIB = os.path.join(PKG, "libdogip.so")
 GEN_OUT = os.path.join(CSRC, "generated", "bhat_gen.cuh")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CU_SOURCES = ["abi.cu", "kernels/apply.cu", "kernels/weights.cu", "kernels/vectors.cu", "kernels/qp.cu"]
+CU_SOURCES = (["abi.cu", "kernels/apply.cu", "kernels/weights.cu", "kernels/vectors.cu", "kernels/qp.cu"] +
+              [f"kernels/apply_{d}_{p}.cu" for d in (2, 3) for p in (1, 2, 3, 4)])
 
 
 def _headers():
@@ -81,7 +82,7 @@ def build(verbose: bool = False, force: bool = False, variant: str = "", defines
         if force or _mtime(o) < max(_mtime(s), hdr_t):
             jobs.append([NVCC] + flags + ["-c", s, "-o", o])
     if jobs:
-        with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
             logs = list(ex.map(_run, jobs))
         with open(os.path.join(build_dir, "ptxas.log"), "w") as f:
             f.write("\n".join(logs))

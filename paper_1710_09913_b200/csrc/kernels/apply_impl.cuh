@@ -1,0 +1,733 @@
+// apply_impl.cuh -- the hot DoGIP apply kernel (sm_100a): templates, included by the
+// per-(d, p) translation units apply_<d>_<p>.cu (compiled in parallel).
+//
+// y += sum_T P_T^T Bhat^T A_T Bhat P_T u      (Algorithm 1, PAPER.md P:491-511;
+//                                              Theorem 2 eq:wp_dogip_mul P:276,
+//                                              Theorem 4 eq:ep_dogip_mul P:439)
+// Mapping:
+//  * one warp = one 32-element tile = 32 consecutive cells along x with the same
+//    simplex type s; one lane = one element;
+//  * the per-element work g = Bhat u_T, h = A_T g, y_T += Bhat^T h is the
+//    generated straight-line, sparsity- and +-1-aware FP64 code of
+//    generated/bhat_gen.cuh, node by node, so only u_T and y_T sit in registers;
+//  * A_T is stored tile-major [tile][W_T * NC][32] (lane fastest) and streamed
+//    by each warp through its own S-stage shared-memory ring with 1D bulk
+//    copies (cp.async.bulk, the TMA engine) that complete on mbarriers; the
+//    stream runs ahead across tile boundaries, so HBM requests stay in flight
+//    independently of register pressure.  Chunk boundaries are compile-time
+//    (node rows), so the refill address is one add off the tile pointer;
+//  * gather/scatter offsets are formed in registers: every simplex of the cell
+//    has v_0 = cell origin, so off(l) = sum_i alpha_i(l) v_i(s) with compile-time
+//    alpha and d per-tile vertex strides (no per-DoF table loads);
+//  * the next tile's u_T is gathered (read-only loads) before this tile's y_T is
+//    scattered with fire-and-forget red.global.add.f64 (y zeroed first), so the
+//    gather latency overlaps the scatter; DIRICHLET zeroes boundary DoFs of u_T
+//    and skips their scatter (the boundary rows are fixed by dirichlet_fixup).
+#pragma once
+#include <cuda_runtime.h>
+
+#ifdef DOGIP_GEN_HEADER
+#include DOGIP_GEN_HEADER
+#else
+#include "../generated/bhat_gen.cuh"
+#endif
+#include "apply.cuh"
+#include "common.cuh"
+
+#ifndef DOGIP_LOCKSTEP
+#define DOGIP_LOCKSTEP -1      // CTA barrier at every weight chunk (the CTA's warps share I-cache
+                               // lines): -1 per-variant policy, 0 never, 1 always (A/B builds)
+#endif
+#ifndef DOGIP_SYM_UPF
+#define DOGIP_SYM_UPF 1        // symmetry-adapted body: stage the next tile's u_T in shared memory
+#endif
+#ifndef DOGIP_STAGES
+#define DOGIP_STAGES 4          // ring stages per warp
+#endif
+#ifndef DOGIP_ROWS_3CTA
+#define DOGIP_ROWS_3CTA 18      // max rows per chunk when 3 CTAs share an SM
+#endif
+#ifndef DOGIP_ROWS_2CTA
+#define DOGIP_ROWS_2CTA 24      // ... when 2 CTAs share an SM
+#endif
+
+namespace dogip {
+
+namespace {
+
+// 3 CTAs (12 warps) per SM where u_T + y_T fit in <= 170 registers, else 2
+#ifndef DOGIP_MINB_LARGE
+#define DOGIP_MINB_LARGE 2   // CTAs/SM asked of ptxas when V_T > 20 (3D P4)
+#endif
+#ifndef DOGIP_MINB_SMALL
+#define DOGIP_MINB_SMALL 3   // CTAs/SM asked of ptxas when V_T <= 10 (2D P1-P3, 3D P1-P2)
+#endif
+#ifndef DOGIP_ROWS_4CTA
+#define DOGIP_ROWS_4CTA 12
+#endif
+#ifndef DOGIP_PAIR_MINB
+#define DOGIP_PAIR_MINB 4    // CTAs/SM of the paired-lane WP kernel (u_T, y_T halves: <= 128 registers)
+#endif
+template <class RE>
+constexpr int min_blocks() {
+#ifdef DOGIP_MINB_OVERRIDE
+    return DOGIP_MINB_OVERRIDE;
+#endif
+    if constexpr (RE::PAIR) return DOGIP_PAIR_MINB;   // paired-lane WP (STORE 3)
+    else return RE::VT <= 10 ? DOGIP_MINB_SMALL : RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE;
+}
+
+// Balanced chunks of whole nodes: NCH = ceil(TILE_ROWS / ROWS_MAX) chunks of ROWS rows
+// (a multiple of NC, so a node's NC rows never straddle two chunks; the NG leading
+// rows of the iso storage sit in chunk 0), the last chunk shorter.
+#ifndef DOGIP_SYM_ROWS
+#define DOGIP_SYM_ROWS 24      // rows per chunk of the symmetry-adapted kernel (u_T staging shares smem)
+#endif
+#ifndef DOGIP_SYM_STAGES
+#define DOGIP_SYM_STAGES 2
+#endif
+#ifndef DOGIP_STAGES_FORCE
+#define DOGIP_STAGES_FORCE 0   // > 0: every kernel uses this many stages (A/B builds)
+#endif
+// Lock-stepping the 4 warps of a CTA at every weight chunk (profiles/r01_ab_lockstep2.log):
+// -5 % for the FP64-bound ISO storage (C4 iso 2.47 -> 2.34 ms, C2 p=4 iso -14 %), -1 % for
+// the long full tiles of C4 / C5; +3 % for the symmetry-adapted kernel, +2 % for C2 p=4 EL
+template <class RE>
+__host__ __device__ constexpr bool lockstep() {
+    if constexpr (DOGIP_LOCKSTEP >= 0) return DOGIP_LOCKSTEP != 0;
+    else return !RE::DOT_IN_BODY && !RE::PAIR && (RE::NG > 0 || RE::TILE_ROWS >= 165);
+}
+
+template <class RE, int TW = TILE>
+struct Chunking {
+    // ring stages per (d, p, form, storage), from the B200 A/B of 2/3/4 stages
+    // (profiles/r01_ab_ring_stages.log): double buffering wins for the long weight tiles of
+    // 3D P3 EL (C4: 3.72 -> 3.45 ms), 2D P4 EL and the symmetry-adapted kernel, 4 stages
+    // for the rest (C2 p=2, C3, C4 iso, C5 full lose 1-6 % with 2)
+    static constexpr int S = DOGIP_STAGES_FORCE > 0 ? DOGIP_STAGES_FORCE
+                           : RE::DOT_IN_BODY ? DOGIP_SYM_STAGES
+                           : (RE::NC > 1 && RE::TILE_ROWS >= 84) ? 2
+                           : DOGIP_STAGES;
+    static constexpr int TILE_ROWS = RE::TILE_ROWS;
+    static constexpr int AL = RE::RALIGN;                                  // chunk boundaries fall on rows % AL == 0
+    // the symmetry-adapted kernel stages u_T in shared memory too: 16-row chunks keep 2 CTAs/SM
+    static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 4 ? DOGIP_ROWS_4CTA
+                                     : min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA
+                                     : (DOGIP_SYM_UPF && RE::DOT_IN_BODY) ? DOGIP_SYM_ROWS : DOGIP_ROWS_2CTA;
+    static constexpr int ROWS_MAX = (ROWS_MAX0 / AL) * AL;
+    static constexpr int NCH0 = (TILE_ROWS + ROWS_MAX - 1) / ROWS_MAX;
+    static constexpr int ROWS_B = (TILE_ROWS + NCH0 - 1) / NCH0;
+    static constexpr int ROWS1 = ((ROWS_B + AL - 1) / AL) * AL;
+    static constexpr int ROWS = ROWS1 < RE::NG + RE::NC ? RE::NG + RE::NC : ROWS1;
+    static constexpr int NCH = (TILE_ROWS + ROWS - 1) / ROWS;             // chunks per tile
+    static constexpr int LAST = TILE_ROWS - (NCH - 1) * ROWS;              // rows of the last chunk
+    static constexpr int64_t TILE_DBL = (int64_t)TILE_ROWS * TW;           // doubles per tile
+    static_assert(RE::NG == 0 || RE::NG <= ROWS, "iso G rows must sit in chunk 0");
+};
+
+template <class RE>
+struct WarpStream {
+    using C = Chunking<RE>;
+    double* ring;          // this warp's ring in shared memory
+    uint32_t bar0;         // smem address of this warp's S mbarriers
+    int lane;
+    const double* tptr;    // weights of the tile being consumed
+    int64_t tstride;       // doubles between this warp's consecutive tiles
+    int64_t tiles_left;    // this warp's tiles from the current one on
+    uint32_t cons;         // chunks consumed so far (stage = cons % S, parity = cons / S)
+    const double* cur;     // current stage + lane
+    uint64_t policy;
+
+    // chunk-sequence number g (relative: K tiles ahead, chunk c) -> stage g % S
+    template <int K, int CI>
+    __device__ __forceinline__ void issue(uint32_t stage) const {   // lane 0 only
+        if (K >= tiles_left) return;
+        constexpr int rows = (CI == C::NCH - 1) ? C::LAST : C::ROWS;
+        constexpr uint32_t bytes = (uint32_t)rows * TILE * 8u;
+        const uint32_t bar = bar0 + 8u * stage;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s_evict_first(smem_u32(ring + (size_t)stage * C::ROWS * TILE),
+                             tptr + K * tstride + (int64_t)CI * C::ROWS * TILE, bytes, bar, policy);
+    }
+    template <int G>
+    __device__ __forceinline__ void prologue_one() {
+        if constexpr (G < C::S - 1) {
+            issue<G / C::NCH, G % C::NCH>((uint32_t)G);
+            prologue_one<G + 1>();
+        }
+    }
+    __device__ __forceinline__ void prologue() { prologue_one<0>(); }
+    // node J's weights start a new chunk (node 0 also covers the NG leading rows)
+    template <int J>
+    __device__ __forceinline__ void begin() {
+        constexpr int c_cur = RE::row_of(J) / C::ROWS;
+        if constexpr (J == 0 || c_cur != RE::row_of(J - 1) / C::ROWS) {
+            constexpr int gi = c_cur + C::S - 1;          // chunk refilled now, relative to this tile
+            if constexpr (lockstep<RE>()) asm volatile("bar.sync 1, %0;" ::"n"(APPLY_THREADS) : "memory");
+            __syncwarp();
+            if (lane == 0) {
+                fence_proxy_async_smem();                 // prior generic reads of the stage
+                issue<gi / C::NCH, gi % C::NCH>((cons + C::S - 1) % C::S);
+            }
+            const uint32_t st = cons % C::S;
+            mbar_wait(bar0 + 8u * st, (cons / C::S) & 1u);
+            cur = ring + (size_t)st * C::ROWS * TILE + lane;
+            ++cons;
+        }
+    }
+    template <int J>
+    __device__ __forceinline__ void end() {}
+    __device__ __forceinline__ double w(int k) const { return cur[(k % C::ROWS) * TILE]; }
+    __device__ __forceinline__ void next_tile() {
+        tptr += tstride;
+        --tiles_left;
+    }
+};
+
+#ifndef DOGIP_DIRECT_ROWS
+#define DOGIP_DIRECT_ROWS 6    // tiles with at most this many weight rows skip the smem ring
+#endif
+template <class RE>
+__host__ __device__ constexpr bool direct_weights() { return !RE::DOT_IN_BODY && !RE::PAIR && RE::TILE_ROWS <= DOGIP_DIRECT_ROWS; }
+
+// weights already in registers (direct-weights path): node rows are compile-time indices
+struct RegPol {
+    const double* wr;
+    template <int J>
+    __device__ __forceinline__ void begin() {}
+    template <int J>
+    __device__ __forceinline__ void end() {}
+    __device__ __forceinline__ double w(int k) const { return wr[k]; }
+};
+
+// LOCKSTEP: a warp with fewer tiles than its CTA's first warp matches the barriers the
+// others still execute (NCH per tile)
+template <class RE, class C>
+__device__ __forceinline__ void lockstep_tail(int64_t gw, int64_t tile_end, int64_t gw0, int64_t nw) {
+    if constexpr (lockstep<RE>()) {
+        const int64_t mine = gw < tile_end ? (tile_end - gw + nw - 1) / nw : 0;
+        const int64_t first = gw0 < tile_end ? (tile_end - gw0 + nw - 1) / nw : 0;
+        for (int64_t k = mine; k < first; ++k)
+            for (int c = 0; c < C::NCH; ++c) asm volatile("bar.sync 1, %0;" ::"n"(APPLY_THREADS) : "memory");
+    }
+}
+
+// Theorem 1 storage (global WP diagonal over W = C_{N,2p}): the weight of
+// double-grid node j of the element is gathered from the global W-lattice vector.
+struct GatherPol {
+    const double* wg;      // global W weights of this slab
+    const int* offw;       // shared-memory W-lattice offsets of this simplex type
+    int64_t baseW;         // W-lattice index of the cell origin
+    template <int J>
+    __device__ __forceinline__ void begin() {}
+    template <int J>
+    __device__ __forceinline__ void end() {}
+    __device__ __forceinline__ double w(int k) const { return __ldg(wg + baseW + offw[k]); }
+};
+
+// Per-tile gather context of one lane's element.
+struct ElemCtx {
+    int64_t base;          // DoF index of the cell origin
+    int v1, v2, v3;        // DoF-lattice offsets of vertices 1..d
+    uint64_t skip;         // bit l: local DoF l is not gathered / scattered (Dirichlet)
+    bool valid;            // lane holds a real element (ci < Nx)
+    int s, ci, cj, ck;
+};
+
+template <class RE, int D, bool DIR>
+__device__ __forceinline__ ElemCtx elem_ctx(const SlabGeo& geo, const ApplyTables& tab, int64_t t, int lane) {
+    const TileCoord tc = tile_coord(geo, t);
+    ElemCtx c;
+    c.s = tc.s; c.ci = tc.ci0 + lane; c.cj = tc.cj; c.ck = tc.ck;
+    c.valid = c.ci < geo.Nx;
+    c.base = (int64_t)geo.p * (c.ci + geo.sy * tc.cj + geo.sz * tc.ck);
+    c.v1 = tab.vstr[tc.s][0];
+    c.v2 = tab.vstr[tc.s][1];
+    c.v3 = D == 3 ? tab.vstr[tc.s][2] : 0;
+    c.skip = 0;
+    if constexpr (DIR) {   // boundary DoFs = DoFs on a cell face that lies on the domain boundary
+        const unsigned long long* fm = tab.fmask[tc.s];
+        uint64_t b = 0;
+        if (c.ci == 0) b |= fm[0];
+        if (c.ci == geo.Nx - 1) b |= fm[1];
+        if (D == 3) {
+            if (tc.cj == 0) b |= fm[2];
+            if (tc.cj == geo.Ny - 1) b |= fm[3];
+            if (tc.ck == 0 && geo.bnd_lo) b |= fm[4];
+            if (tc.ck == geo.Nz - 1 && geo.bnd_hi) b |= fm[5];
+        } else {
+            if (tc.cj == 0 && geo.bnd_lo) b |= fm[2];
+            if (tc.cj == geo.Ny - 1 && geo.bnd_hi) b |= fm[3];
+        }
+        c.skip = b;
+    }
+    return c;
+}
+
+template <class RE, int L>
+__device__ __forceinline__ int dof_off(const ElemCtx& c) {
+    return RE::ALPHA[L][0] * c.v1 + RE::ALPHA[L][1] * c.v2 + RE::ALPHA[L][2] * c.v3;
+}
+
+template <class RE, int L = 0>
+__device__ __forceinline__ void gather(const double* __restrict__ u, const ElemCtx& c, double* uT) {
+    if constexpr (L < RE::VT) {
+        const bool take = c.valid && !((c.skip >> L) & 1ull);
+        uT[L] = take ? ldg_f64(u + c.base + dof_off<RE, L>(c)) : 0.0;
+        gather<RE, L + 1>(u, c, uT);
+    }
+}
+
+// u_T of a tile -> the warp's [VT][32] shared buffer with cp.async (no registers held)
+template <class RE, int L = 0>
+__device__ __forceinline__ void gather_async(const double* __restrict__ u, const ElemCtx& c, uint32_t ubuf_lane) {
+    if constexpr (L < RE::VT) {
+        if (c.valid && !((c.skip >> L) & 1ull)) cp_async8(ubuf_lane + 8u * TILE * L, u + c.base + dof_off<RE, L>(c));
+        gather_async<RE, L + 1>(u, c, ubuf_lane);
+    }
+}
+
+template <class RE, int L = 0>
+__device__ __forceinline__ void scatter(double* __restrict__ y, const ElemCtx& c, const double* yT) {
+    if constexpr (L < RE::VT) {
+        if (!((c.skip >> L) & 1ull)) red_add_f64(y + c.base + dof_off<RE, L>(c), yT[L]);
+        scatter<RE, L + 1>(y, c, yT);
+    }
+}
+
+template <int D, int P, int F, int ST, bool DIR, bool GLOB>
+__global__ void __launch_bounds__(APPLY_THREADS, min_blocks<dogip_gen::RefElem<D, P, F, ST>>())
+apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
+             const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end,
+             double* __restrict__ dot_partials, const int* __restrict__ offw_g) {
+    using RE = dogip_gen::RefElem<D, P, F, ST>;
+    using C = Chunking<RE>;
+    constexpr int NW = APPLY_THREADS / 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* rings = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)NW * C::S * C::ROWS * TILE);
+    constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
+    double* ubufs = reinterpret_cast<double*>(bars + NW * C::S);            // [NW][VT][32] (UPF only)
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t gw = tile_begin + (int64_t)blockIdx.x * NW + warp;
+    const int64_t nw = (int64_t)gridDim.x * NW;
+    WarpStream<RE> ws;
+    ws.ring = rings + (size_t)warp * C::S * C::ROWS * TILE;
+    ws.bar0 = smem_u32(bars + warp * C::S);
+    ws.lane = lane;
+    ws.tptr = w + gw * C::TILE_DBL;
+    ws.tstride = nw * C::TILE_DBL;
+    ws.tiles_left = gw < tile_end ? (tile_end - gw + nw - 1) / nw : 0;
+    ws.cons = 0;
+    ws.policy = policy_evict_first();
+    __shared__ int offw_s[GLOB ? MAX_NS * MAX_WT_GLOBAL : 1];
+    constexpr bool DW = direct_weights<RE>() && !GLOB;
+    if constexpr (GLOB) {
+        for (int i = threadIdx.x; i < MAX_NS * RE::WT; i += blockDim.x)
+            offw_s[(i / RE::WT) * MAX_WT_GLOBAL + i % RE::WT] = offw_g[i];
+        __syncthreads();
+    } else if (DW) {
+    } else if (lane == 0) {
+        for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
+        fence_mbar_init();
+        ws.prologue();                                   // prologue of the weight stream
+    }
+    __syncwarp();
+
+    double udot = 0.0;
+    double uT[RE::VT];
+    ElemCtx cur{};
+    if constexpr (DW) {
+        // tiny tiles (<= DOGIP_DIRECT_ROWS weight rows): each lane reads its element's
+        // weights with coalesced read-only loads (one 256 B row per warp load), the next
+        // tile's together with its u_T gather -- no ring, barriers or bulk copies
+        double wr[RE::TILE_ROWS];
+        auto loadw = [&](int64_t t) {
+            const double* wt = w + t * C::TILE_DBL + lane;
+#pragma unroll
+            for (int k = 0; k < RE::TILE_ROWS; ++k) wr[k] = ldg_stream_f64(wt + k * TILE);
+        };
+        if (gw < tile_end) {
+            cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
+            gather<RE>(u, cur, uT);
+            loadw(gw);
+        }
+        for (int64_t tile = gw; tile < tile_end; tile += nw) {
+            double yT[RE::VT];
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
+            RegPol rp{wr};
+            RE::body(uT, yT, rp);
+            if (dot_partials) {
+#pragma unroll
+                for (int l = 0; l < RE::VT; ++l) udot = fma(uT[l], yT[l], udot);
+            }
+            const ElemCtx prev = cur;
+            if (tile + nw < tile_end) {
+                cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
+                gather<RE>(u, cur, uT);
+                loadw(tile + nw);
+            }
+            if (prev.valid) scatter<RE>(y, prev, yT);
+        }
+    } else if constexpr (UPF) {
+        double* ubuf = ubufs + (size_t)warp * RE::VT * TILE;
+        const uint32_t ubuf_lane = smem_u32(ubuf + lane);
+        if (gw < tile_end) {
+            cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
+            gather_async<RE>(u, cur, ubuf_lane);
+        }
+        cp_async_commit();
+        for (int64_t tile = gw; tile < tile_end; tile += nw) {
+            cp_async_wait_all();
+            __syncwarp();
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l)
+                uT[l] = (cur.valid && !((cur.skip >> l) & 1ull)) ? ubuf[l * TILE + lane] : 0.0;
+            __syncwarp();
+            const ElemCtx prev = cur;
+            if (tile + nw < tile_end) {         // next tile's u_T lands in smem during this body
+                cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
+                gather_async<RE>(u, cur, ubuf_lane);
+            }
+            cp_async_commit();
+            double yT[RE::VT];
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
+            if constexpr (RE::DOT_IN_BODY) RE::body(uT, yT, ws, dot_partials ? &udot : nullptr);
+            ws.next_tile();
+            if (prev.valid) scatter<RE>(y, prev, yT);
+        }
+        lockstep_tail<RE, C>(gw, tile_end, tile_begin + (int64_t)blockIdx.x * NW, nw);
+    } else {
+    if (gw < tile_end) {
+        cur = elem_ctx<RE, D, DIR>(geo, tab, gw, lane);
+        gather<RE>(u, cur, uT);
+    }
+    for (int64_t tile = gw; tile < tile_end; tile += nw) {
+        double yT[RE::VT];
+#pragma unroll
+        for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
+        if constexpr (GLOB) {
+            GatherPol gp{w, offw_s + cur.s * MAX_WT_GLOBAL,
+                         (int64_t)(2 * geo.p) * (cur.ci + geo.swy * cur.cj + geo.swz * cur.ck)};
+            RE::body(uT, yT, gp);
+        } else {
+            if constexpr (RE::DOT_IN_BODY) RE::body(uT, yT, ws, dot_partials ? &udot : nullptr);
+            else RE::body(uT, yT, ws);
+            ws.next_tile();
+        }
+        // u^T A u = sum_T u_T^T (Bhat^T A_T Bhat u_T): the CG dot p.q, element by element
+        // (padding lanes and Dirichlet DoFs have u_T = 0 and contribute nothing)
+        if (!RE::DOT_IN_BODY && dot_partials) {
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) udot = fma(uT[l], yT[l], udot);
+        }
+        const ElemCtx prev = cur;
+        if (tile + nw < tile_end) {            // next tile's gather overlaps this scatter
+            cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
+            gather<RE>(u, cur, uT);
+        }
+        if (prev.valid) scatter<RE>(y, prev, yT);
+    }
+    if constexpr (!GLOB) lockstep_tail<RE, C>(gw, tile_end, tile_begin + (int64_t)blockIdx.x * NW, nw);
+    }
+    if (dot_partials) {     // deterministic: one partial per warp, fixed order reduction later
+        for (int o = 16; o > 0; o >>= 1) udot += __shfl_xor_sync(0xffffffffu, udot, o);
+        if (lane == 0) dot_partials[(int64_t)blockIdx.x * NW + warp] = udot;
+    }
+}
+
+// ------------------------------------------------------------------ paired lanes
+// WP with two lanes per element (generated RefElem<D,P,0,3>, see gen_bhat.cpp
+// emit_pair): lane 2e+k holds the view slots of element e of a 16-element
+// half-tile; weights are stored per half-tile [ht][row][16] with node pairs in
+// adjacent rows.  Halves the registers of u_T and y_T (3D P4: 19 + 19 doubles
+// instead of 35 + 35), doubling the resident warps of the FP64-heavy C5 body.
+constexpr int PTW = 16;     // elements per half-tile
+
+template <class RE>
+struct PairStream {
+    using C = Chunking<RE, PTW>;
+    double* ring;
+    uint32_t bar0;
+    int lane, col, k;      // col = element column e, k = lane parity
+    const double* tptr;
+    int64_t tstride, tiles_left;
+    uint32_t cons;
+    const double* cself;   // row 2i + k of the current stage (column col)
+    const double* cother;  // row 2i + 1 - k
+    const double* cfix;    // row r
+    uint64_t policy;
+
+    template <int K, int CI>
+    __device__ __forceinline__ void issue(uint32_t stage) const {
+        if (K >= tiles_left) return;
+        constexpr int rows = (CI == C::NCH - 1) ? C::LAST : C::ROWS;
+        constexpr uint32_t bytes = (uint32_t)rows * PTW * 8u;
+        const uint32_t bar = bar0 + 8u * stage;
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s_evict_first(smem_u32(ring + (size_t)stage * C::ROWS * PTW),
+                             tptr + K * tstride + (int64_t)CI * C::ROWS * PTW, bytes, bar, policy);
+    }
+    template <int G>
+    __device__ __forceinline__ void prologue_one() {
+        if constexpr (G < C::S - 1) {
+            issue<G / C::NCH, G % C::NCH>((uint32_t)G);
+            prologue_one<G + 1>();
+        }
+    }
+    __device__ __forceinline__ void prologue() { prologue_one<0>(); }
+    template <int R>
+    __device__ __forceinline__ void begin() {
+        constexpr int c_cur = R / C::ROWS;
+        if constexpr (R == 0 || c_cur != (R - 1) / C::ROWS) {
+            constexpr int gi = c_cur + C::S - 1;
+            __syncwarp();
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                issue<gi / C::NCH, gi % C::NCH>((cons + C::S - 1) % C::S);
+            }
+            const uint32_t st = cons % C::S;
+            mbar_wait(bar0 + 8u * st, (cons / C::S) & 1u);
+            cfix = ring + (size_t)st * C::ROWS * PTW + col;
+            cself = cfix + k * PTW;
+            cother = cfix + (1 - k) * PTW;
+            ++cons;
+        }
+    }
+    __device__ __forceinline__ double wself(int r) const { return cself[(r % C::ROWS) * PTW]; }
+    __device__ __forceinline__ double wother(int r) const { return cother[(r % C::ROWS) * PTW]; }
+    __device__ __forceinline__ double wfix(int r) const { return cfix[(r % C::ROWS) * PTW]; }
+    __device__ __forceinline__ double xchg(double v) const { return __shfl_xor_sync(0xffffffffu, v, 1); }
+    __device__ __forceinline__ void next_tile() {
+        tptr += tstride;
+        --tiles_left;
+    }
+};
+
+struct PairCtx {
+    int64_t base;          // DoF index of this lane's view origin (cell origin + p V_0)
+    int w1, w2, w3;        // DoF offsets per unit of alpha_1..alpha_d in this lane's view
+    bool valid;
+};
+
+template <class RE, int D>
+__device__ __forceinline__ PairCtx pair_ctx(const SlabGeo& geo, const ApplyTables& tab, int64_t ht, int col, int k) {
+    const TileCoord tc = tile_coord(geo, ht >> 1);
+    const int ci = tc.ci0 + PTW * (int)(ht & 1) + col;
+    PairCtx c;
+    c.valid = ci < geo.Nx;
+    // lane 1 sees DoF sigma(alpha): off = sum_j alpha_j V_{sigma j}, V_0 = 0 (cell origin),
+    // alpha_0 = p - sum_{j>=1} alpha_j  ->  base + p V'_0 + sum_{j>=1} alpha_j (V'_j - V'_0)
+    const int V[4] = {0, tab.vstr[tc.s][0], tab.vstr[tc.s][1], D == 3 ? tab.vstr[tc.s][2] : 0};
+    int Vk[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Vk[j] = k ? V[RE::sigma(j)] : V[j];
+    c.base = (int64_t)geo.p * (ci + geo.sy * tc.cj + geo.sz * tc.ck) + (int64_t)geo.p * Vk[0];
+    c.w1 = Vk[1] - Vk[0];
+    c.w2 = Vk[2] - Vk[0];
+    c.w3 = D == 3 ? Vk[3] - Vk[0] : 0;
+    return c;
+}
+
+template <class RE, int M>
+__device__ __forceinline__ int pair_off(const PairCtx& c) {
+    return RE::SLOT_ALPHA[M][0] * c.w1 + RE::SLOT_ALPHA[M][1] * c.w2 + RE::SLOT_ALPHA[M][2] * c.w3;
+}
+
+template <class RE, int M = 0>
+__device__ __forceinline__ void pair_gather(const double* __restrict__ ub, const PairCtx& c, double* U) {
+    if constexpr (M < RE::VS) {
+        U[M] = ldg_f64(ub + pair_off<RE, M>(c));
+        pair_gather<RE, M + 1>(ub, c, U);
+    }
+}
+
+// lane 1 does not scatter the fixed slots (both lanes hold their complete sums)
+template <class RE, int M = 0>
+__device__ __forceinline__ void pair_scatter(double* __restrict__ yb, const PairCtx& c, const double* Y, int k) {
+    if constexpr (M < RE::VS) {
+        if (M < RE::VS - RE::NFIX || k == 0) red_add_f64(yb + pair_off<RE, M>(c), Y[M]);
+        pair_scatter<RE, M + 1>(yb, c, Y, k);
+    }
+}
+
+template <int D, int P>
+__global__ void __launch_bounds__(APPLY_THREADS, min_blocks<dogip_gen::RefElem<D, P, 0, 3>>())
+apply_pair_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
+                  const SlabGeo geo, const ApplyTables tab, const int64_t ht_begin, const int64_t ht_end,
+                  double* __restrict__ dot_partials) {
+    using RE = dogip_gen::RefElem<D, P, 0, 3>;
+    using C = Chunking<RE, PTW>;
+    constexpr int NW = APPLY_THREADS / 32;
+    constexpr int VS = RE::VS, NA = RE::VS - RE::NFIX;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* rings = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)NW * C::S * C::ROWS * PTW);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int col = lane >> 1, k = lane & 1;
+    const int64_t gw = ht_begin + (int64_t)blockIdx.x * NW + warp;
+    const int64_t nw = (int64_t)gridDim.x * NW;
+    PairStream<RE> ws;
+    ws.ring = rings + (size_t)warp * C::S * C::ROWS * PTW;
+    ws.bar0 = smem_u32(bars + warp * C::S);
+    ws.lane = lane; ws.col = col; ws.k = k;
+    ws.tptr = w + gw * C::TILE_DBL;
+    ws.tstride = nw * C::TILE_DBL;
+    ws.tiles_left = gw < ht_end ? (ht_end - gw + nw - 1) / nw : 0;
+    ws.cons = 0;
+    ws.policy = policy_evict_first();
+    if (lane == 0) {
+        for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
+        fence_mbar_init();
+        ws.prologue();
+    }
+    __syncwarp();
+
+    double udot = 0.0;
+    double U[VS];
+    PairCtx cur{};
+    auto gather = [&](const PairCtx& c) {
+#pragma unroll
+        for (int m = 0; m < VS; ++m) U[m] = 0.0;
+        if (c.valid) pair_gather<RE>(u + c.base, c, U);
+    };
+    if (gw < ht_end) {
+        cur = pair_ctx<RE, D>(geo, tab, gw, col, k);
+        gather(cur);
+    }
+    for (int64_t ht = gw; ht < ht_end; ht += nw) {
+        double Y[VS];
+#pragma unroll
+        for (int m = 0; m < VS; ++m) Y[m] = 0.0;
+        RE::body(U, Y, ws);
+        ws.next_tile();
+        if (dot_partials) {   // u_T^T y_T: A slots once per lane, fixed slots half in each lane
+#pragma unroll
+            for (int m = 0; m < VS; ++m) udot = fma(m < NA ? U[m] : 0.5 * U[m], Y[m], udot);
+        }
+        const PairCtx prev = cur;
+        if (ht + nw < ht_end) {
+            cur = pair_ctx<RE, D>(geo, tab, ht + nw, col, k);
+            gather(cur);
+        }
+        if (prev.valid) pair_scatter<RE>(y + prev.base, prev, Y, k);
+    }
+    if (dot_partials) {
+        for (int o = 16; o > 0; o >>= 1) udot += __shfl_xor_sync(0xffffffffu, udot, o);
+        if (lane == 0) dot_partials[(int64_t)blockIdx.x * NW + warp] = udot;
+    }
+}
+
+template <int D, int P>
+cudaError_t launch_pair(const ApplyArgs& a) {
+    using RE = dogip_gen::RefElem<D, P, 0, 3>;
+    using C = Chunking<RE, PTW>;
+    constexpr int NW = APPLY_THREADS / 32;
+    const size_t smem = (size_t)NW * C::S * C::ROWS * PTW * 8 + (size_t)NW * C::S * 8;
+    auto kern = apply_pair_kernel<D, P>;
+    static int configured = 0;
+    static int occ = 1;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, APPLY_THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        configured = 1;
+    }
+    const int64_t h0 = 2 * a.tile_begin, h1 = 2 * a.tile_end;     // half-tiles
+    const int64_t nht = h1 - h0;
+    int64_t grid = (int64_t)a.num_sms * occ;
+    const int64_t need = (nht + NW - 1) / NW;
+    if (grid > need) grid = need;
+    if (a.dot_partials) {
+        if (grid < 1) grid = 1;
+        if (grid * NW > APPLY_MAX_WARPS) grid = APPLY_MAX_WARPS / NW;
+        *a.dot_nslots = (int)(grid * NW);
+    } else if (nht <= 0) {
+        return cudaSuccess;
+    }
+    kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, h0, h1, a.dot_partials);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+template <int D, int P, int F, int ST, bool DIR, bool GLOB>
+cudaError_t launch_one(const ApplyArgs& a) {
+    using RE = dogip_gen::RefElem<D, P, F, ST>;
+    using C = Chunking<RE>;
+    constexpr int NW = APPLY_THREADS / 32;
+    constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
+    constexpr bool DW = direct_weights<RE>() && !GLOB;
+    const size_t smem = (GLOB || DW) ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8 +
+                                   (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0);
+    auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
+    static int configured = 0;   // per instantiation
+    static int occ = 1;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, APPLY_THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        configured = 1;
+    }
+    const int64_t ntiles = a.tile_end - a.tile_begin;
+    int64_t grid = (int64_t)a.num_sms * occ;
+    const int64_t need = (ntiles + NW - 1) / NW;
+    if (grid > need) grid = need;
+    if (a.dot_partials) {       // every slot of the partial array must be written
+        if (grid < 1) grid = 1;
+        if (grid * NW > APPLY_MAX_WARPS) grid = APPLY_MAX_WARPS / NW;
+        *a.dot_nslots = (int)(grid * NW);
+    } else if (ntiles <= 0) {
+        return cudaSuccess;
+    }
+    kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, a.tile_begin,
+                                                           a.tile_end, a.dot_partials, a.offw);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+template <int D, int P, int F, int ST>
+cudaError_t launch_dir(const ApplyArgs& a) {
+    return a.dirichlet ? launch_one<D, P, F, ST, true, false>(a) : launch_one<D, P, F, ST, false, false>(a);
+}
+
+template <int D, int P>
+cudaError_t launch_form(const ApplyArgs& a) {
+    if (a.form == 0 && a.store == 2) return launch_one<D, P, 0, 0, false, true>(a);   // WP has no BC
+    if (a.form == 0 && a.store == 3) return launch_pair<D, P>(a);
+    if (a.form == 0 && a.store == 5) return launch_one<D, P, 0, 5, false, false>(a);
+    if (a.form == 0) return launch_dir<D, P, 0, 0>(a);
+    return a.store == 1 ? launch_dir<D, P, 1, 1>(a) : launch_dir<D, P, 1, 0>(a);
+}
+
+// Reference-element constants of the generated tables, for the host side.
+template <int D, int P, int F, int ST>
+void fill_info(RefInfo& r) {
+    using RE = dogip_gen::RefElem<D, P, F, ST>;
+    r.VT = RE::VT; r.WT = RE::WT; r.NC = RE::NC; r.NG = RE::NG; r.NS = RE::NS;
+    r.tile_rows = RE::TILE_ROWS;
+    r.flops = RE::FLOPS; r.nnz = RE::NNZ; r.nnz_pm1 = RE::NNZ_PM1;
+    r.pair = RE::PAIR;
+    r.sym = ST == 5;
+    if constexpr (ST == 5) {
+        for (int j = 0; j < RE::WT; ++j)
+            for (int k = 0; k < 4; ++k) { r.symj[j][k] = RE::SYMJ[j][k]; r.symc[j][k] = RE::SYMC[j][k]; }
+    }
+    for (int j = 0; j < RE::WT && j < MAX_WT_GLOBAL; ++j) {
+        if constexpr (RE::PAIR) r.rowperm[j] = RE::ROWPERM[j];
+        else r.rowperm[j] = j;
+    }
+    for (int s = 0; s < RE::NS; ++s)
+        for (int l = 0; l < RE::VT; ++l)
+            for (int ax = 0; ax < 3; ++ax) r.loff[s][l][ax] = ax < D ? RE::LOFF[s][l][ax] : 0;
+}
+
+}  // namespace
+}  // namespace dogip
