@@ -1,6 +1,6 @@
 // vectors.cu -- CG vector kernels, reductions and boundary handling (sm_100a).
 //
-// CG (reading L15, Hestenes-Stiefel) needs per iteration: q = A p (apply.cu),
+// CG (reading L15, Hestenes-Stiefel) needs per iteration: q = A p (apply_impl.cuh),
 // p.q, x += alpha p, r -= alpha q with r.r, p = r + beta p.  The scalars stay
 // on the device (scal[]), so an iteration enqueues without host round trips;
 // alpha / beta are formed inside the kernels.  Reductions are deterministic:
