@@ -444,7 +444,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         a.symj = dj;
         a.symc = dc;
     }
-    if (a.pair) {
+    if (a.pair || op->ref.has_rowperm) {
         int* drp = nullptr;
         if (tmp.alloc(&drp, WT)) return cleanup_fail(DOGIP_E_OOM, "row permutation");
         cudaMemcpy(drp, op->ref.rowperm, sizeof(int) * WT, cudaMemcpyHostToDevice);
@@ -1124,7 +1124,7 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
             for (int j = 0; j < WT; ++j)
                 for (int c = 0; c < NC; ++c)
                     host[(e * WT + j) * NC + c] =
-                        op->store == DOGIP_STORE_ISO ? at(op->ref.NG + j) * at(c) : at(j * NC + c);
+                        op->store == DOGIP_STORE_ISO ? at(op->ref.NG + op->ref.rowperm[j]) * at(c) : at(j * NC + c);
         }
     return DOGIP_OK;
 }

@@ -100,7 +100,7 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
     auto simp = cell_simplices(d);
     auto A = multi_indices(d, p);
     std::fprintf(f, "template <> struct RefElem<%d, %d, %d, %d> {\n", d, p, form, store);
-    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = %d, NG = %d, ROWS = %d, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 0;\n",
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = %d, NG = %d, ROWS = %d, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 0, HAS_ROWPERM = 0;\n",
                  VT, WT, NC, NG, ROWS, TILE_ROWS, (int)simp.size(), NC);
     std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
     std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
@@ -271,7 +271,7 @@ static void emit_pair(FILE* f, int d, int p) {
     for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
     auto simp = cell_simplices(d);
     std::fprintf(f, "template <> struct RefElem<%d, %d, 0, 3> {\n", d, p);
-    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = 2, PAIR = 1, DOT_IN_BODY = 0;\n",
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = 2, PAIR = 1, DOT_IN_BODY = 0, HAS_ROWPERM = 1;\n",
                  VT, WT, WT, (int)simp.size());
     std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
     std::fprintf(f, "    static constexpr int VS = %d, NFIX = %d, NPAIR = %d;\n", VS, NFIX, NPAIR);
@@ -485,7 +485,7 @@ static void emit_sym(FILE* f, int d, int p) {
     for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
     auto simp = cell_simplices(d);
     std::fprintf(f, "template <> struct RefElem<%d, %d, 0, 5> {\n", d, p);
-    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 1;\n",
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 1, HAS_ROWPERM = 0;\n",
                  VT, WT, WT, (int)simp.size(), NGR);
     std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d, NGROUP = %d;\n", nnz, pm1, NGR);
     std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
@@ -677,10 +677,232 @@ static void emit_sym(FILE* f, int d, int p) {
     std::fprintf(f, "};\n\n");
 }
 
+// Symmetry-adapted body of the isotropic EL storage (STORE 1, corollary P:411-428):
+// sigma = (1 2) swaps xhat_1 <-> xhat_2, i.e. the gradient components r = 0 <-> 1, and
+// Bhat_EL is equivariant, Bhat[s r][sigma j][sigma l] = Bhat[r][j][l].  With
+// v+ = u_l + u_{sigma l}, v- = u_l - u_{sigma l} (DoF pairs) the gradients of a node pair
+// (j, jj = sigma j) are g_r(j) = P_r + Q_r, g_{s r}(jj) = P_r - Q_r with P_r from the
+// even and Q_r from the odd half of row (r, j) -- each half has ~1/3 fewer nonzeros
+// (3D P3: 690 instead of 1014).  The weights act in the original basis (h = a_j G g),
+// then H+/-_r = h_r(j) +/- h_{s r}(jj) feed the transposed halves; y_l, y_{sigma l} are
+// recovered from the even / odd accumulators.  Node pairs are stored in adjacent rows.
+static void emit_iso_sym(FILE* f, int d, int p) {
+    Table t = bhat_table(d, p, 1);
+    const int VT = t.cols, WT = t.rows;
+    const int NSYM = d * (d + 1) / 2, NG = NSYM;
+    auto A = multi_indices(d, p);
+    auto W = multi_indices(d, 2 * p - 2);
+    const int sig[4] = {0, 2, 1, 3};       // barycentric lambda_1 <-> lambda_2
+    const int sr[3] = {1, 0, 2};           // gradient components
+    auto perm = [&](const std::array<int, 4>& a) {
+        std::array<int, 4> b{};
+        for (int i = 0; i <= d; ++i) b[i] = a[sig[i]];
+        return b;
+    };
+    auto find = [](const std::vector<std::array<int, 4>>& v, const std::array<int, 4>& a) {
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i] == a) return (int)i;
+        std::fprintf(stderr, "iso-sym: not found\n");
+        std::exit(1);
+    };
+    std::vector<int> sA(VT), sW(WT);
+    for (int l = 0; l < VT; ++l) sA[l] = find(A, perm(A[l]));
+    for (int j = 0; j < WT; ++j) sW[j] = find(W, perm(W[j]));
+    for (int r = 0; r < d; ++r)
+        for (int j = 0; j < WT; ++j)
+            for (int l = 0; l < VT; ++l)
+                if (t.at(sr[r], sW[j], sA[l]) != t.at(r, j, l)) { std::fprintf(stderr, "iso-sym: not equivariant\n"); std::exit(1); }
+    std::vector<std::pair<int, int>> vp;   // DoF pairs (l < sigma l)
+    std::vector<int> vf;                   // fixed DoFs
+    for (int l = 0; l < VT; ++l) {
+        if (sA[l] > l) vp.push_back({l, sA[l]});
+        else if (sA[l] == l) vf.push_back(l);
+    }
+    std::vector<std::pair<int, int>> wp;   // node pairs
+    std::vector<int> wf;
+    for (int j = 0; j < WT; ++j) {
+        if (sW[j] > j) wp.push_back({j, sW[j]});
+        else if (sW[j] == j) wf.push_back(j);
+    }
+    // storage rows: G (NG rows), then node pairs adjacent, then fixed nodes
+    std::vector<int> rowperm(WT);
+    int nr = 0;
+    for (auto& pr : wp) { rowperm[pr.first] = nr++; rowperm[pr.second] = nr++; }
+    for (int j : wf) rowperm[j] = nr++;
+    // adapted coordinates: vs[i], vd[i] for pair i; u[vf] directly
+    const int NP = (int)vp.size(), NF = (int)vf.size();
+    int nnz = 0, pm1 = 0;
+    for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
+    auto simp = cell_simplices(d);
+    std::fprintf(f, "template <> struct RefElem<%d, %d, 1, 1> {\n", d, p);
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = %d, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = 1, PAIR = 0, DOT_IN_BODY = 0, HAS_ROWPERM = 1;\n",
+                 VT, WT, NG, NG + WT, (int)simp.size());
+    std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
+    std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
+    for (size_t si = 0; si < simp.size(); ++si) {
+        std::fprintf(f, "%s{", si ? ", " : "");
+        for (int l = 0; l < VT; ++l) {
+            std::fprintf(f, "%s{", l ? "," : "");
+            for (int ax = 0; ax < d; ++ax) {
+                int o = 0;
+                for (int i = 0; i <= d; ++i) o += A[l][i] * simp[si][i][ax];
+                std::fprintf(f, "%s%d", ax ? "," : "", o);
+            }
+            std::fprintf(f, "}");
+        }
+        std::fprintf(f, "}");
+    }
+    std::fprintf(f, "};\n");
+    std::fprintf(f, "    static constexpr signed char ALPHA[%d][3] = {", VT);
+    for (int l = 0; l < VT; ++l)
+        std::fprintf(f, "%s{%d,%d,%d}", l ? "," : "", A[l][1], A[l][2], d == 3 ? A[l][3] : 0);
+    std::fprintf(f, "};\n");
+    std::fprintf(f, "    static constexpr short ROWPERM[%d] = {", WT);
+    for (int j = 0; j < WT; ++j) std::fprintf(f, "%s%d", j ? "," : "", rowperm[j]);
+    std::fprintf(f, "};\n");
+    std::fprintf(f, "    static __host__ __device__ constexpr int row_of(int r) { return r; }\n");
+    std::fprintf(f,
+        "    template <class Pol>\n"
+        "    static __device__ __forceinline__ void body(const double* __restrict__ u,\n"
+        "                                                double* __restrict__ y, Pol& pol) {\n");
+    int flops = 0;
+    int idx[3][3], c = 0;
+    for (int r = 0; r < d; ++r)
+        for (int s2 = r; s2 < d; ++s2) { idx[r][s2] = idx[s2][r] = c++; }
+    // inputs: v[0..NP) = u_l + u_sl, v[NP..2NP) = u_l - u_sl, v[2NP + k] = u_{vf[k]}
+    std::fprintf(f, "        double v[%d], zs[%d], zd[%d], zf[%d];\n", VT, NP > 0 ? NP : 1, NP > 0 ? NP : 1, NF > 0 ? NF : 1);
+    for (int i = 0; i < NP; ++i) {
+        std::fprintf(f, "        v[%d] = u[%d] + u[%d];\n        v[%d] = u[%d] - u[%d];\n", i, vp[i].first, vp[i].second,
+                     NP + i, vp[i].first, vp[i].second);
+        flops += 2;
+    }
+    for (int k = 0; k < NF; ++k) std::fprintf(f, "        v[%d] = u[%d];\n", 2 * NP + k, vf[k]);
+    std::fprintf(f, "#pragma unroll\n        for (int k = 0; k < %d; ++k) { zs[k] = 0.0; zd[k] = 0.0; }\n", NP > 0 ? NP : 1);
+    std::fprintf(f, "#pragma unroll\n        for (int k = 0; k < %d; ++k) zf[k] = 0.0;\n", NF > 0 ? NF : 1);
+    std::fprintf(f, "        pol.template begin<0>();\n");
+    for (int k = 0; k < NSYM; ++k) std::fprintf(f, "        const double G%d = pol.w(%d);\n", k, k);
+    // row (r, j) in adapted inputs: even part over vs (+ fixed DoFs), odd part over vd
+    auto even_terms = [&](int r, int j) {
+        std::vector<std::pair<int, Rat>> terms;
+        for (int i = 0; i < NP; ++i) {
+            const Rat cc = (t.at(r, j, vp[i].first) + t.at(r, j, vp[i].second)) * Rat(1, 2);
+            if (!cc.is_zero()) terms.push_back({i, cc});
+        }
+        for (int k = 0; k < NF; ++k)
+            if (!t.at(r, j, vf[k]).is_zero()) terms.push_back({2 * NP + k, t.at(r, j, vf[k])});
+        return terms;
+    };
+    auto odd_terms = [&](int r, int j) {
+        std::vector<std::pair<int, Rat>> terms;
+        for (int i = 0; i < NP; ++i) {
+            const Rat cc = (t.at(r, j, vp[i].first) - t.at(r, j, vp[i].second)) * Rat(1, 2);
+            if (!cc.is_zero()) terms.push_back({NP + i, cc});
+        }
+        return terms;
+    };
+    auto weights = [&](const std::string& a, const std::string& g, const std::string& h) {
+        // h = a * G * g (G symmetric, upper triangle G0..)
+        for (int s2 = 0; s2 < d; ++s2) std::fprintf(f, "          const double t%s%d = %s * %s%d;\n", h.c_str(), s2, a.c_str(), g.c_str(), s2);
+        flops += d;
+        for (int r = 0; r < d; ++r) {
+            std::string acc = "G" + std::to_string(idx[r][0]) + " * t" + h + "0";
+            for (int s2 = 1; s2 < d; ++s2)
+                acc = "__fma_rn(G" + std::to_string(idx[r][s2]) + ", t" + h + std::to_string(s2) + ", " + acc + ")";
+            std::fprintf(f, "          const double %s%d = %s;\n", h.c_str(), r, acc.c_str());
+            flops += 2 * d - 1;
+        }
+    };
+    // projection of original-basis contributions (r, j, value) into zs / zd / zf
+    auto project_even = [&](int r, int j, const std::string& val) {
+        for (int i = 0; i < NP; ++i) {
+            const Rat cc = (t.at(r, j, vp[i].first) + t.at(r, j, vp[i].second)) * Rat(1, 2);
+            if (cc.is_zero()) continue;
+            std::fprintf(f, "          zs[%d] = __fma_rn(%s, %s, zs[%d]);\n", i, lit(cc.to_double()).c_str(), val.c_str(), i);
+            flops += 2;
+        }
+        for (int k = 0; k < NF; ++k) {
+            const Rat cc = t.at(r, j, vf[k]);
+            if (cc.is_zero()) continue;
+            std::fprintf(f, "          zf[%d] = __fma_rn(%s, %s, zf[%d]);\n", k, lit(cc.to_double()).c_str(), val.c_str(), k);
+            flops += 2;
+        }
+    };
+    auto project_odd = [&](int r, int j, const std::string& val) {
+        for (int i = 0; i < NP; ++i) {
+            const Rat cc = (t.at(r, j, vp[i].first) - t.at(r, j, vp[i].second)) * Rat(1, 2);
+            if (cc.is_zero()) continue;
+            std::fprintf(f, "          zd[%d] = __fma_rn(%s, %s, zd[%d]);\n", i, lit(cc.to_double()).c_str(), val.c_str(), i);
+            flops += 2;
+        }
+    };
+    for (size_t q = 0; q < wp.size(); ++q) {
+        const int j = wp[q].first, jj = wp[q].second;
+        const int r0 = NG + rowperm[j];
+        // both rows opened in order: with an odd NG (2D) a pair can straddle two chunks;
+        // aj is read before the second begin may move to the next stage
+        std::fprintf(f, "        {\n          pol.template begin<%d>();\n", r0);
+        std::fprintf(f, "          const double aj = pol.w(%d);\n", r0);
+        std::fprintf(f, "          pol.template begin<%d>();\n", r0 + 1);
+        std::fprintf(f, "          const double ajj = pol.w(%d);\n", r0 + 1);
+        for (int r = 0; r < d; ++r) {
+            flops += emit_combo(f, "          ", "P" + std::to_string(r), true, even_terms(r, j), "v");
+            flops += emit_combo(f, "          ", "Q" + std::to_string(r), true, odd_terms(r, j), "v");
+        }
+        // g(j)_r = P_r + Q_r ; g(jj)_s = P_{sr s} - Q_{sr s}
+        for (int r = 0; r < d; ++r) std::fprintf(f, "          const double ga%d = P%d + Q%d;\n", r, r, r);
+        for (int s2 = 0; s2 < d; ++s2) std::fprintf(f, "          const double gb%d = P%d - Q%d;\n", s2, sr[s2], sr[s2]);
+        flops += 2 * d;
+        weights("aj", "ga", "ha");
+        weights("ajj", "gb", "hb");
+        // H+_r = ha_r + hb_{sr r}, H-_r = ha_r - hb_{sr r}
+        for (int r = 0; r < d; ++r) {
+            std::fprintf(f, "          const double Hp%d = ha%d + hb%d, Hm%d = ha%d - hb%d;\n", r, r, sr[r], r, r, sr[r]);
+            flops += 2;
+        }
+        // pair contribution: y_l + y_sl = sum_r (B_l + B_sl) H+_r (even, fixed DoFs: B_f H+_r),
+        //                    y_l - y_sl = sum_r (B_l - B_sl) H-_r
+        for (int r = 0; r < d; ++r) project_even(r, j, "Hp" + std::to_string(r));
+        for (int r = 0; r < d; ++r) project_odd(r, j, "Hm" + std::to_string(r));
+        std::fprintf(f, "        }\n");
+    }
+    for (int j : wf) {
+        const int r0 = NG + rowperm[j];
+        std::fprintf(f, "        {\n          pol.template begin<%d>();\n", r0);
+        std::fprintf(f, "          const double aj = pol.w(%d);\n", r0);
+        for (int r = 0; r < d; ++r) {
+            flops += emit_combo(f, "          ", "P" + std::to_string(r), true, even_terms(r, j), "v");
+            flops += emit_combo(f, "          ", "Q" + std::to_string(r), true, odd_terms(r, j), "v");
+            std::fprintf(f, "          const double ga%d = P%d + Q%d;\n", r, r, r);
+            flops += 1;
+        }
+        weights("aj", "ga", "ha");
+        // original-basis projection of h(j): y_l = sum_r B_l h_r, y_sl = sum_r B_sl h_r
+        for (int r = 0; r < d; ++r) {
+            project_even(r, j, "ha" + std::to_string(r));
+            project_odd(r, j, "ha" + std::to_string(r));
+        }
+        std::fprintf(f, "        }\n");
+    }
+    // y_l = zs + zd, y_sl = zs - zd, y_f = zf  (the 1/2 of the averages is in the constants:
+    // zs = (y_l + y_sl)/2, zd = (y_l - y_sl)/2)
+    for (int i = 0; i < NP; ++i) {
+        std::fprintf(f, "        y[%d] += zs[%d] + zd[%d];\n        y[%d] += zs[%d] - zd[%d];\n", vp[i].first, i, i,
+                     vp[i].second, i, i);
+        flops += 4;
+    }
+    for (int k = 0; k < NF; ++k) { std::fprintf(f, "        y[%d] += zf[%d];\n", vf[k], k); flops += 1; }
+    std::fprintf(f, "    }\n");
+    std::fprintf(f, "    static constexpr int FLOPS = %d;\n", flops);
+    std::fprintf(f, "};\n\n");
+}
+
+static int g_iso_sym = 0;   // argv[5]: 1 = symmetry-adapted ISO body (measured slower: spills, see DESIGN)
+
 int main(int argc, char** argv) {
     if (argc < 2) { std::fprintf(stderr, "usage: gen_bhat out.cuh [group_values]\n"); return 2; }
     if (argc > 2) g_gmax_vals = std::atoi(argv[2]);
     if (argc > 3) g_split = std::atoi(argv[3]);
+    if (argc > 5) g_iso_sym = std::atoi(argv[5]);
     FILE* f = std::fopen(argv[1], "w");
     if (!f) { std::perror("open"); return 1; }
     std::fprintf(f,
@@ -700,7 +922,8 @@ int main(int argc, char** argv) {
         for (int p = 1; p <= 4; ++p) {
             emit_variant(f, d, p, 0, 0);
             emit_variant(f, d, p, 1, 0);
-            emit_variant(f, d, p, 1, 1);
+            if (g_iso_sym) emit_iso_sym(f, d, p);
+            else emit_variant(f, d, p, 1, 1);
             emit_pair(f, d, p);
             emit_sym(f, d, p);
         }

@@ -58,7 +58,8 @@ struct RefInfo {
     int VT, WT, NC, NG, NS, tile_rows, flops, nnz, nnz_pm1;
     int pair;                        // paired-lane WP layout (STORE 3): half-tiles of 16, rows permuted
     int loff[MAX_NS][MAX_VT][3];
-    int rowperm[MAX_WT_GLOBAL];      // storage row of canonical node j (identity unless pair)
+    int has_rowperm;                 // node rows stored permuted (PAIR, symmetry-adapted ISO)
+    int rowperm[MAX_WT_GLOBAL];      // storage row of canonical node j (identity unless has_rowperm)
     int sym;                         // symmetry-adapted WP (STORE 5): row r = sum_k symc[r][k] a_{symj[r][k]}
     int symj[MAX_WT_GLOBAL][4];
     double symc[MAX_WT_GLOBAL][4];

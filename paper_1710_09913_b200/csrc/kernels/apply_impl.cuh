@@ -720,8 +720,9 @@ void fill_info(RefInfo& r) {
         for (int j = 0; j < RE::WT; ++j)
             for (int k = 0; k < 4; ++k) { r.symj[j][k] = RE::SYMJ[j][k]; r.symc[j][k] = RE::SYMC[j][k]; }
     }
+    r.has_rowperm = RE::HAS_ROWPERM;
     for (int j = 0; j < RE::WT && j < MAX_WT_GLOBAL; ++j) {
-        if constexpr (RE::PAIR) r.rowperm[j] = RE::ROWPERM[j];
+        if constexpr (RE::HAS_ROWPERM) r.rowperm[j] = RE::ROWPERM[j];
         else r.rowperm[j] = j;
     }
     for (int s = 0; s < RE::NS; ++s)

@@ -165,7 +165,7 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
             }
         for (int j = 0; j < WT; ++j) {
             const double aj = direct ? adet * cconst[0] * a.sW[j] : a.scratch_a[el * WT + j];
-            out[(size_t)(a.NG + j) * TILE] = G.valid ? aj : 0.0;
+            out[(size_t)(a.NG + (a.rowperm ? a.rowperm[j] : j)) * TILE] = G.valid ? aj : 0.0;
         }
         return;
     }
