@@ -239,7 +239,7 @@ def run_product(args, cfg) -> None:
     dirichlet = form == 1
     coef = cfg.coefficient()
     mesh = Mesh(cfg.d, cfg.N, cfg.p, cfg.vertices(), rank=rank, nranks=world, nccl_id=nccl_id, device=local)
-    storage = 1 if (args.storage == "iso" and form == 1) else 0
+    storage = 1 if (args.storage == "iso" and form == 1) else 5 if (args.storage == "sym" and form == 0) else 0
     op = Operator(mesh, form, coef, storage=storage)
     info, oinfo = mesh.info, op.info
     stream = torch.cuda.current_stream()
@@ -274,7 +274,7 @@ def run_product(args, cfg) -> None:
 
     # algorithmic bytes of one apply on this rank: streamed weights of
     # real elements + u read once + y written once
-    n_w = oinfo["W_T"] * oinfo["n_c"] if storage == 0 else oinfo["W_T"] + oinfo["n_c"]
+    n_w = oinfo["W_T"] + oinfo["n_c"] if storage == 1 else oinfo["W_T"] * oinfo["n_c"]
     alg_bytes = 8 * n_w * info["n_elem_local"] + 16 * info["ndof_local"]
     flops_apply = oinfo["flops_per_elem"] * info["n_elem_local"]
     peak, peak_src = _measured_peaks()
@@ -371,9 +371,10 @@ def main():
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the secondary ISO-storage measurement")
-    ap.add_argument("--storage", default="full", choices=["full", "iso"],
-                    help="EL weight storage: full symmetric blocks (P:443) or the isotropic "
-                         "compression of the corollary P:411-428 (a_{T,j} R^-1 R^-T)")
+    ap.add_argument("--storage", default="full", choices=["full", "iso", "sym"],
+                    help="weight storage: full (P:281 / P:443), iso = EL isotropic compression of "
+                         "the corollary P:411-428 (a_{T,j} R^-1 R^-T), sym = WP symmetry-adapted "
+                         "(DOGIP_STORE_SYM, e.g. --config C5 --storage sym)")
     args = ap.parse_args()
     from synth.configs import get_config
     cfg = get_config(args.config)
