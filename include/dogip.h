@@ -209,10 +209,13 @@ int dogip_weights(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_
 
 /* dogip_weights with an explicit storage variant (DOGIP_STORE_*).  DOGIP_STORE_ISO
  * needs form = DOGIP_EL (else E_INVALID_ARG) and an isotropic coefficient kind
- * (else E_BAD_COEFF); DOGIP_STORE_GLOBAL needs form = DOGIP_WP (else
- * E_INVALID_ARG).  The apply result is the same operator up to rounding.
- * dogip_export_weights of a GLOBAL op returns, per element, the stored values of
- * its W nodes, A_{l^W_T(j), l^W_T(j)} / mult_{l^W_T(j)}. */
+ * (else E_BAD_COEFF); DOGIP_STORE_GLOBAL, _PAIR and _SYM need form = DOGIP_WP (else
+ * E_INVALID_ARG); DOGIP_STORE_QP takes both forms and stores no weights.  The apply
+ * result is the same operator up to rounding for every storage.
+ * dogip_export_weights returns a_{T,j} / A_{T,j} in canonical order for FULL, ISO,
+ * PAIR and SYM (converted back from the stored layout), per element the stored values
+ * of its W nodes, A_{l^W_T(j), l^W_T(j)} / mult_{l^W_T(j)}, for GLOBAL, and
+ * E_INVALID_ARG for QP. */
 int dogip_weights_ex(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_n1d, int storage,
                      void* stream, dogip_op* out);
 
