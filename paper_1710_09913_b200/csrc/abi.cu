@@ -303,6 +303,20 @@ static int sum_interface_planes(dogip_mesh_s* m, double* v, int64_t P, int64_t n
     return DOGIP_OK;
 }
 
+// Coefficient parameters as the kernels read them: the caller's array, plus for the
+// rotated anisotropic field cos(phi) and sin(phi) of its 3n phases appended (so each point
+// needs one sincos per Fourier mode, geometry.cuh coef_eval).
+static std::vector<double> device_params(const dogip_coeff* c) {
+    std::vector<double> v(c->params, c->params + c->nparams);
+    if (c->kind == DOGIP_COEF_ANISO_FOURIER && c->nparams >= 4) {
+        const int n = (int)c->params[3];
+        const double* phi = c->params + 4 + 3 * n;
+        for (int i = 0; i < 3 * n; ++i) v.push_back((double)std::cos((long double)phi[i]));
+        for (int i = 0; i < 3 * n; ++i) v.push_back((double)std::sin((long double)phi[i]));
+    }
+    return v;
+}
+
 struct DevBufs {   // frees on scope exit
     std::vector<void*> p;
     ~DevBufs() { for (void* x : p) cudaFree(x); }
@@ -369,6 +383,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     }
     op->w_doubles = storage == DOGIP_STORE_QP ? 0 : m->geo.ntiles * (int64_t)op->ref.tile_rows * TILE;
     auto cleanup_fail = [&](int code, const std::string& msg) { dogip_op_destroy(op); return fail(code, msg); };
+    const std::vector<double> qparams = device_params(coeff);
     if (storage == DOGIP_STORE_QP) {
         // matrix-free comparator: basis values / reference gradients at the n_q points of
         // the same rule, coefficient parameters and per-cell values; nothing per element
@@ -382,7 +397,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         if (!up(&op->d_sV, sV.data(), VT) || !up(&op->q_pts, pts.data(), pts.size()) ||
             !up(&op->q_wts, wts.data(), wts.size()) || !up(&op->q_phi, phiV.data(), phiV.size()) ||
             !up(&op->q_dphi, dphiV.data(), dphiV.size()) ||
-            !up(&op->q_params, coeff->params, (size_t)coeff->nparams))
+            !up(&op->q_params, qparams.data(), qparams.size()))
             return cleanup_fail(DOGIP_E_OOM, "quadrature tables");
         if (coeff->kind == DOGIP_COEF_PER_CELL && !up(&op->q_cell, coeff->per_cell, (size_t)ipow(m->N, d)))
             return cleanup_fail(DOGIP_E_OOM, "per-cell coefficient");
@@ -416,10 +431,10 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     a.stream = st;
     double *dparams = nullptr, *dqp = nullptr, *dqw = nullptr, *dphi = nullptr, *dsW = nullptr, *dcell = nullptr;
     int* dbad = nullptr;
-    if (tmp.alloc(&dparams, coeff->nparams) || tmp.alloc(&dqp, pts.size()) || tmp.alloc(&dqw, wts.size()) ||
+    if (tmp.alloc(&dparams, qparams.size()) || tmp.alloc(&dqp, pts.size()) || tmp.alloc(&dqw, wts.size()) ||
         tmp.alloc(&dphi, phiW.size()) || tmp.alloc(&dsW, WT) || tmp.alloc(&dbad, 1))
         return cleanup_fail(DOGIP_E_OOM, "weight tables");
-    if (coeff->nparams) cudaMemcpy(dparams, coeff->params, sizeof(double) * coeff->nparams, cudaMemcpyHostToDevice);
+    if (!qparams.empty()) cudaMemcpy(dparams, qparams.data(), sizeof(double) * qparams.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(dqp, pts.data(), sizeof(double) * pts.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(dqw, wts.data(), sizeof(double) * wts.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(dphi, phiW.data(), sizeof(double) * phiW.size(), cudaMemcpyHostToDevice);

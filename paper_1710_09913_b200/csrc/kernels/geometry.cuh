@@ -144,12 +144,18 @@ __device__ __forceinline__ void coef_eval(int kind, const double* P, const doubl
         case DOGIP_COEF_ANISO_FOURIER: {
             const int n = (int)P[3];
             const double* kap = P + 4;
-            const double* phi = P + 4 + 3 * n;
             const double* cc = P + 4 + 6 * n;
             double w[3] = {0.0, 0.0, 0.0};
             for (int m = 0; m < n; ++m) {
+                // cos(arg + phi_i) = cos(arg) cos(phi_i) - sin(arg) sin(phi_i): one sincos per
+                // mode instead of three cos (the phases are per-parameter constants)
                 const double arg = 2.0 * M_PI * (x[0] * kap[3 * m] + x[1] * kap[3 * m + 1] + x[2] * kap[3 * m + 2]);
-                for (int i = 0; i < 3; ++i) w[i] += cc[3 * m + i] * cos(arg + phi[3 * m + i]);
+                double sa, ca;
+                sincos(arg, &sa, &ca);
+                const double* cphi = P + 4 + 9 * n;      // cos / sin of the phases (appended by
+                const double* sphi = cphi + 3 * n;       // the host, abi.cu device_params)
+#pragma unroll
+                for (int i = 0; i < 3; ++i) w[i] += cc[3 * m + i] * (ca * cphi[3 * m + i] - sa * sphi[3 * m + i]);
             }
             double R[3][3];
             const double t = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
