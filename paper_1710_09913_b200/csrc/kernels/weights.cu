@@ -5,7 +5,8 @@
 // with the collapsed Gauss-Jacobi rule Q (reading L10).  Three steps per batch
 // of elements (K-order = apply-kernel tile order):
 //   1. quad_coef : C[e, c, q] = |det R_T| w_q M_c(F_T xq)      (c = coefficient component)
-//   2. gemm      : Abar[e, c, j] = sum_q C[e, c, q] Phi[q, j]   (smem-tiled FP64 DMMA GEMM)
+//   2. gemm      : Abar[j, e, c] = sum_q C[e, c, q] Phi[q, j]   (smem-tiled FP64 DMMA GEMM,
+//                  stored transposed so step 3 reads it coalesced along e)
 //   3. finalize  : congruence with Rinv_T (EL) and the tile-major store [tile][j*NC+c][lane]
 // Cell-constant coefficients skip 1-2: Abar = |det R_T| M_T s_j, s_j = sum_q w_q phi^W_j(xq).
 #include <cuda_runtime.h>
@@ -47,14 +48,14 @@ __global__ void quad_coef_kernel(WeightsArgs a, int64_t e0, int64_t nb) {
     if (G.valid && !ok) atomicOr(a.bad_flag, 2);
 }
 
-// 2. C (M x N) = A^T (K x M)^T * B (K x N), row-major, FP64 on the FP64 tensor path
+// 2. C^T (N x M) with C = A^T (K x M)^T * B (K x N), FP64 on the FP64 tensor path
 //    (mma.sync.aligned.m8n8k4.f64, DMMA -- sm_100a has no tcgen05 f64 kind): block tile
 //    64 (M) x 56 (N), 4 warps each owning 2 x 7 m8n8 accumulator tiles, K in steps of
 //    16 through padded shared memory (row stride 68 / 60 doubles: a fragment load is the
 //    optimal 2 wavefronts).  N = W_T: 165 (C5) -> 3 column blocks of 56 (2 % padding).
 constexpr int GBM = 64, GBN = 56, GK = 16, GPA = GBM + 4, GPB = GBN + 4;
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 __global__ void __launch_bounds__(128) gemm_kernel(const double* __restrict__ AT, const double* __restrict__ B,
@@ -62,8 +63,11 @@ __global__ void __launch_bounds__(128) gemm_kernel(const double* __restrict__ AT
     __shared__ __align__(16) double As[GK][GPA];
     __shared__ __align__(16) double Bs[GK][GPB];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t m0 = (int64_t)blockIdx.x * GBM;
-    const int n0 = blockIdx.y * GBN;
+    // column tile fastest: the NT CTAs sharing one A row block run together, so the
+    // block is read from DRAM once and re-read from L2 (not NT times from DRAM)
+    const int NT = (N + GBN - 1) / GBN;
+    const int64_t m0 = (int64_t)(blockIdx.x / NT) * GBM;
+    const int n0 = (int)(blockIdx.x % NT) * GBN;
     double acc[2][7][2] = {};
     // register-staged double buffering: the next K slab's global loads are in flight
     // while this slab's DMMAs run
@@ -127,7 +131,7 @@ __global__ void __launch_bounds__(128) gemm_kernel(const double* __restrict__ AT
             for (int h = 0; h < 2; ++h) {
                 const int64_t gm = m0 + (warp * 2 + mt) * 8 + (lane >> 2);
                 const int gn = n0 + nt * 8 + 2 * (lane & 3) + h;
-                if (gm < M && gn < N) C[gm * N + gn] = acc[mt][nt][h];
+                if (gm < M && gn < N) C[(int64_t)gn * M + gm] = acc[mt][nt][h];   // C^T: [n][m]
             }
 }
 
@@ -164,13 +168,13 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
                 ++o;
             }
         for (int j = 0; j < WT; ++j) {
-            const double aj = direct ? adet * cconst[0] * a.sW[j] : a.scratch_a[el * WT + j];
+            const double aj = direct ? adet * cconst[0] * a.sW[j] : a.scratch_a[(size_t)j * nb + el];
             out[(size_t)(a.NG + (a.rowperm ? a.rowperm[j] : j)) * TILE] = G.valid ? aj : 0.0;
         }
         return;
     }
     if (a.sym) {   // symmetry-adapted WP rows: ahat_psi(P) = (1/s) sum_c psi(c) a_{c j0} (STORE 5)
-        auto aj = [&](int j) { return direct ? adet * cconst[0] * a.sW[j] : a.scratch_a[el * WT + j]; };
+        auto aj = [&](int j) { return direct ? adet * cconst[0] * a.sW[j] : a.scratch_a[(size_t)j * nb + el]; };
         for (int r = 0; r < WT; ++r) {
             double v = 0.0;
             for (int k = 0; k < 4; ++k) {
@@ -184,7 +188,7 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
     for (int j = 0; j < WT; ++j) {
         double ab[6];
         for (int c = 0; c < nc; ++c)
-            ab[c] = direct ? adet * cconst[c] * a.sW[j] : a.scratch_a[(el * nc + c) * WT + j];
+            ab[c] = direct ? adet * cconst[c] * a.sW[j] : a.scratch_a[(size_t)j * nb * nc + el * nc + c];
         if (a.pair) {
             out[(size_t)a.rowperm[j] * 16] = G.valid ? ab[0] : 0.0;
             continue;
@@ -234,7 +238,7 @@ cudaError_t launch_weights(const WeightsArgs& a) {
             if (a.d == 2) quad_coef_kernel<2><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb);
             else quad_coef_kernel<3><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb);
             const int64_t M = nb * a.ncomp;
-            dim3 grid((unsigned)((M + GBM - 1) / GBM), (unsigned)((a.WT + GBN - 1) / GBN));
+            const unsigned grid = (unsigned)(((M + GBM - 1) / GBM) * ((a.WT + GBN - 1) / GBN));
             gemm_kernel<<<grid, 128, 0, a.stream>>>(a.scratch_c, a.phiW, a.scratch_a, M, a.WT, a.nq);
         }
         if (a.d == 2) finalize_kernel<2><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb, direct ? 1 : 0);
