@@ -86,10 +86,19 @@ static int emit_combo(FILE* f, const char* indent, const std::string& dst, bool 
 // interpolated values per emission group (argv[2]); 1 = node by node, which measured
 // best on B200 (profiles/r01_ab_variants.log: grouping 12 values was neutral-to-worse)
 static int g_gmax_vals = 1;
+// EL bodies through the barycentric derivatives (argv[6]; default 0 = off): per node
+//   t_i = sum_l D_i[j,l] u_l (i = 0..d),  g_r = t_{r+1} - t_0,
+//   y_l += sum_{i>=1} D_i[j,l] h_{i-1} - D_0[j,l] (h_0 + .. + h_{d-1})
+// = the Bhat_EL body exactly (Bhat_r = D_{r+1} - D_0), with 3D P3 740 instead of 1014
+// table nonzeros per direction (tables.hpp bary_deriv_table).
+static int g_bary = 0;   // measured slower on B200 (spills; profiles/r01_ab_bary_deriv.log)
 
 static void emit_variant(FILE* f, int d, int p, int form, int store) {
     Table t = bhat_table(d, p, form);
     const int VT = t.cols, WT = t.rows;
+    const bool bary = form == 1 && g_bary;
+    Table D;
+    if (bary) D = bary_deriv_table(d, p);
     const int NSYM = d * (d + 1) / 2;
     const int NC = (form == 0 || store == 1) ? 1 : NSYM;
     const int NG = store == 1 ? NSYM : 0;
@@ -154,13 +163,31 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
         std::fprintf(f, "        {\n");
         for (int j = j0; j < j1; ++j)
             if (!(store == 1 && j == 0)) std::fprintf(f, "          pol.template begin<%d>();\n", j);
-        for (int j = j0; j < j1; ++j)
+        for (int j = j0; j < j1; ++j) {
+            if (bary) {
+                const std::string sj = "_" + std::to_string(j);
+                bool t0 = false;
+                for (int i = 0; i <= d; ++i) {
+                    std::vector<std::pair<int, Rat>> terms;
+                    for (int l = 0; l < VT; ++l)
+                        if (!D.at(i, j, l).is_zero()) terms.push_back({l, D.at(i, j, l)});
+                    if (i == 0) t0 = !terms.empty();
+                    flops += emit_combo(f, "          ", "t" + std::to_string(i) + "b" + sj, true, terms, "u");
+                }
+                for (int r = 0; r < d; ++r) {
+                    if (t0) std::fprintf(f, "          const double g%d%s = t%db%s - t0b%s;\n", r, sj.c_str(), r + 1, sj.c_str(), sj.c_str());
+                    else std::fprintf(f, "          const double g%d%s = t%db%s;\n", r, sj.c_str(), r + 1, sj.c_str());
+                    flops += t0;
+                }
+                continue;
+            }
             for (int b = 0; b < t.nblk; ++b) {
                 std::vector<std::pair<int, Rat>> terms;
                 for (int l = 0; l < VT; ++l)
                     if (!t.at(b, j, l).is_zero()) terms.push_back({l, t.at(b, j, l)});
                 flops += emit_combo(f, "          ", "g" + std::to_string(b) + "_" + std::to_string(j), true, terms, "u");
             }
+        }
         for (int j = j0; j < j1; ++j) {
             const std::string sj = "_" + std::to_string(j);
             if (form == 0) {
@@ -188,6 +215,32 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
                     std::fprintf(f, "          const double h%d%s = %s;\n", r, sj.c_str(), acc.c_str());
                     flops += 2 * d - 1;
                 }
+            }
+            if (bary) {
+                bool d0 = false;
+                for (int l = 0; l < VT; ++l) d0 |= !D.at(0, j, l).is_zero();
+                if (d0) {
+                    std::string s = "h0" + sj;
+                    for (int r = 1; r < d; ++r) s += " + h" + std::to_string(r) + sj;
+                    std::fprintf(f, "          const double hs%s = %s;\n", sj.c_str(), s.c_str());
+                    flops += d - 1;
+                }
+                for (int l = 0; l < VT; ++l) {
+                    std::string acc = "y[" + std::to_string(l) + "]";
+                    bool any = false;
+                    for (int i = 0; i <= d; ++i) {
+                        Rat cv = i == 0 ? Rat(0) - D.at(0, j, l) : D.at(i, j, l);
+                        if (cv.is_zero()) continue;
+                        any = true;
+                        std::string h = i == 0 ? "hs" + sj : "h" + std::to_string(i - 1) + sj;
+                        if (cv == Rat(1)) acc = "(" + acc + ") + " + h;
+                        else if (cv == Rat(-1)) acc = "(" + acc + ") - " + h;
+                        else { acc = "__fma_rn(" + lit(cv.to_double()) + ", " + h + ", " + acc + ")"; flops += 1; }
+                        flops += 1;
+                    }
+                    if (any) std::fprintf(f, "          y[%d] = %s;\n", l, acc.c_str());
+                }
+                continue;
             }
             for (int l = 0; l < VT; ++l) {
                 std::string acc = "y[" + std::to_string(l) + "]";
@@ -903,6 +956,7 @@ int main(int argc, char** argv) {
     if (argc > 2) g_gmax_vals = std::atoi(argv[2]);
     if (argc > 3) g_split = std::atoi(argv[3]);
     if (argc > 5) g_iso_sym = std::atoi(argv[5]);
+    if (argc > 6) g_bary = std::atoi(argv[6]);
     FILE* f = std::fopen(argv[1], "w");
     if (!f) { std::perror("open"); return 1; }
     std::fprintf(f,

@@ -166,6 +166,29 @@ inline Table bhat_table(int d, int p, int form) {
     return t;
 }
 
+// Barycentric partial derivatives D_i[j][l] = d phi^l_V / d lambda_i (xhat^j_W), i = 0..d,
+// at the EL double-grid nodes (2p-2 lattice); Bhat_EL block r = D_{r+1} - D_0 (reading
+// L2).  Each D_i is sparser than the difference (one lambda factor differentiated),
+// so the generated EL body interpolates through them.
+inline Table bary_deriv_table(int d, int p) {
+    Table t;
+    auto A = multi_indices(d, p);
+    auto W = nodes_bary(d, 2 * p - 2);
+    t.nblk = d + 1;
+    t.rows = (int)W.size();
+    t.cols = (int)A.size();
+    t.v.resize((size_t)t.nblk * t.rows * t.cols);
+    for (int i = 0; i <= d; ++i)
+        for (int j = 0; j < t.rows; ++j)
+            for (int l = 0; l < t.cols; ++l) {
+                Rat v = dfactor(A[l][i], p, W[j][i]);
+                for (int m = 0; m <= d; ++m)
+                    if (m != i) v = v * factor(A[l][m], p, W[j][m]);
+                t.v[((size_t)i * t.rows + j) * t.cols + l] = v;
+            }
+    return t;
+}
+
 // ------------------------------------------------- float evaluation (points)
 // Basis of P_k at reference points (long double product formula).
 inline void eval_basis_ld(int d, int k, const double* pts, int npts, double* out /* npts x dim */) {
