@@ -21,7 +21,7 @@ namespace {
 
 // 1. CT[q][e*ncomp + c] = |det| w_q M_c(x_q)   (element index fastest: coalesced stores,
 //    and the GEMM's A operand read along M)
-template <int D>
+template <int D, int KIND>
 __global__ void quad_coef_kernel(WeightsArgs a, int64_t e0, int64_t nb) {
     // one thread per element (geometry once), looping over the points; for a fixed point
     // consecutive threads write consecutive elements
@@ -40,7 +40,7 @@ __global__ void quad_coef_kernel(WeightsArgs a, int64_t e0, int64_t nb) {
             for (int c = 0; c < D; ++c) x[r] += G.R[r][c] * a.qp[q * D + c];
         }
         double cv[6];
-        coef_eval<D>(a.kind, a.params, a.per_cell, G.cell, x, cv);
+        coef_eval<D>(KIND < 0 ? a.kind : KIND, a.params, a.per_cell, G.cell, x, cv);   // switch folded per KIND
         ok = ok && coef_ok(a.ncomp, D, cv);
         const double sc = adet * a.qw[q];
         for (int c = 0; c < a.ncomp; ++c) a.scratch_c[(int64_t)q * M + el * a.ncomp + c] = sc * cv[c];
@@ -235,8 +235,16 @@ cudaError_t launch_weights(const WeightsArgs& a) {
     for (int64_t e0 = 0; e0 < nel; e0 += a.batch) {
         const int64_t nb = (nel - e0) < a.batch ? (nel - e0) : a.batch;
         if (!direct) {
-            if (a.d == 2) quad_coef_kernel<2><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb);
-            else quad_coef_kernel<3><<<(unsigned)((nb + 127) / 128), 128, 0, a.stream>>>(a, e0, nb);
+            const unsigned qb = (unsigned)((nb + 127) / 128);
+            if (a.d == 2) {
+                if (a.kind == DOGIP_COEF_SINCOS2D) quad_coef_kernel<2, DOGIP_COEF_SINCOS2D><<<qb, 128, 0, a.stream>>>(a, e0, nb);
+                else if (a.kind == DOGIP_COEF_TANH_RADIAL) quad_coef_kernel<2, DOGIP_COEF_TANH_RADIAL><<<qb, 128, 0, a.stream>>>(a, e0, nb);
+                else quad_coef_kernel<2, -1><<<qb, 128, 0, a.stream>>>(a, e0, nb);
+            } else {
+                if (a.kind == DOGIP_COEF_TANH_RADIAL) quad_coef_kernel<3, DOGIP_COEF_TANH_RADIAL><<<qb, 128, 0, a.stream>>>(a, e0, nb);
+                else if (a.kind == DOGIP_COEF_ANISO_FOURIER) quad_coef_kernel<3, DOGIP_COEF_ANISO_FOURIER><<<qb, 128, 0, a.stream>>>(a, e0, nb);
+                else quad_coef_kernel<3, -1><<<qb, 128, 0, a.stream>>>(a, e0, nb);
+            }
             const int64_t M = nb * a.ncomp;
             const unsigned grid = (unsigned)(((M + GBM - 1) / GBM) * ((a.WT + GBN - 1) / GBN));
             gemm_kernel<<<grid, 128, 0, a.stream>>>(a.scratch_c, a.phiW, a.scratch_a, M, a.WT, a.nq);
