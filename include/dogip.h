@@ -24,6 +24,12 @@
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Work is asynchronous on that stream, except dogip_cg and the *_host
  *    entry points, which synchronise it.
+ *  - Concurrency: an op is read-only after dogip_weights, so single-rank
+ *    dogip_apply calls on one op may run concurrently on different streams
+ *    with distinct y.  Calls that use library-owned scratch are
+ *    NOT re-entrant per handle: dogip_apply_host and dogip_cg (per op), and
+ *    any call that exchanges interface planes (nranks > 1, per mesh) --
+ *    serialise those on one stream / thread per handle.
  *  - Multi-GPU (nranks > 1): one process per GPU; every call is collective and
  *    must be made by all ranks in the same order.  The mesh is split into
  *    slabs of whole cube layers along the LAST axis (z in 3D, y in 2D); rank r
