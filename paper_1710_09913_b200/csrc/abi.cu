@@ -143,6 +143,9 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
     g.Nz = d == 2 ? 1 : (int)L;
     g.nxb = (int)((N + TILE - 1) / TILE);
     g.ntiles = (int64_t)g.ns * g.nxb * g.Ny * g.Nz;
+    g.fd_ns = make_fastdiv((uint32_t)g.ns);
+    g.fd_nxb = make_fastdiv((uint32_t)g.nxb);
+    g.fd_ny = make_fastdiv((uint32_t)g.Ny);
     if (2 * g.ntiles >= (int64_t)1 << 31) {   // tile_coord's 32-bit arithmetic (half-tiles of PAIR)
         delete m;
         return fail(DOGIP_E_INVALID_SIZE, "invalid-size: more than 2^30 element tiles per rank");

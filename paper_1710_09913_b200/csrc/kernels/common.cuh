@@ -12,6 +12,23 @@ constexpr int MAX_NS = 6;      // 3! Kuhn simplices per cube
 // Geometry of this rank's slab as seen by the kernels.  Cells (ci, cj, ck)
 // are LOCAL (ck in [0, Nz) along the slab axis; 2D: ck = 0, cj along the slab
 // axis).  DoF lattice strides sx = 1, sy = M, sz = M^2, M = pN + 1.
+// q = n / d for 0 <= n < 2^31 as one wide multiply and a shift (round-up method:
+// m = ceil(2^(31+l) / d), l = ceil(log2 d), so m < 2^32 and floor(n m / 2^(31+l)) is
+// exact for 31-bit n).  Replaces the ~20-instruction runtime integer division in the
+// per-tile coordinate decode, which dominated the 2D P1 kernel's instruction count.
+struct FastDiv {
+    uint32_t m;
+    int sh;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    return FastDiv{(uint32_t)(((1ull << (31 + l)) + d - 1) / d), 31 + l};
+}
+__device__ __host__ __forceinline__ uint32_t fdiv(uint32_t n, FastDiv f) {
+    return (uint32_t)(((uint64_t)n * f.m) >> f.sh);
+}
+
 struct SlabGeo {
     int d, p, ns;                  // dimension, order, simplices per cell
     int Nx, Ny, Nz;                // local cells per axis (2D: Nz = 1)
@@ -25,6 +42,7 @@ struct SlabGeo {
     int N;                         // global cells per axis
     int64_t swy, swz;              // W-lattice (order 2p) strides of the global WP storage
     int64_t ndof_w;                // local W-lattice DoFs
+    FastDiv fd_ns, fd_nxb, fd_ny;  // divisors of tile_coord (set with the fields above)
 };
 
 // Tile t -> (simplex s, x-block, cj, ck).  Tiles are ordered with s fastest,
@@ -38,13 +56,13 @@ struct TileCoord {
 __device__ __host__ inline TileCoord tile_coord(const SlabGeo& g, int64_t t64) {
     TileCoord c;
     const uint32_t t = (uint32_t)t64, ns = (uint32_t)g.ns, nxb = (uint32_t)g.nxb;
-    const uint32_t r1 = t / ns;
+    const uint32_t r1 = fdiv(t, g.fd_ns);
     c.s = (int)(t - r1 * ns);
-    const uint32_t r2 = r1 / nxb;
+    const uint32_t r2 = fdiv(r1, g.fd_nxb);
     const int xb = (int)(r1 - r2 * nxb);
     if (g.d == 3) {
         const uint32_t ny = (uint32_t)g.Ny;
-        const uint32_t ck = r2 / ny;
+        const uint32_t ck = fdiv(r2, g.fd_ny);
         c.cj = (int)(r2 - ck * ny);
         c.ck = (int)ck;
     } else {
