@@ -73,7 +73,8 @@ def test_slab_ranges_tile_the_axis(N, n):
     assert max(b - a for a, b in z) - min(b - a for a, b in z) <= 1
 
 
-@pytest.mark.parametrize("d,N,p,nranks", [(2, 5, 2, 1), (2, 33, 1, 1), (3, 3, 3, 1), (3, 4, 2, 2), (2, 6, 3, 3)])
+@pytest.mark.parametrize("d,N,p,nranks", [(2, 5, 2, 1), (2, 33, 1, 1), (3, 3, 3, 1), (3, 4, 2, 2), (2, 6, 3, 3),
+                                          (3, 33, 1, 2), (2, 97, 2, 3)])
 def test_host_mesh_info_and_dofmap(d, N, p, nranks):
     lT = om.dof_map(om.structured_mesh(d, N), p)
     ns = 2 if d == 2 else 6
@@ -100,6 +101,17 @@ def test_mesh_argument_errors(args, code):
     with pytest.raises(DogipError) as ei:
         Mesh(*args, device=-1)
     assert ei.value.code == code
+
+
+def test_mesh_tile_count_limit():
+    """More than 2^30 element tiles per rank (tile_coord's 31-bit multiply-shift decode)
+    is rejected at setup, before any allocation."""
+    with pytest.raises(DogipError) as ei:
+        Mesh(3, 2048, 1, device=-1)
+    assert ei.value.code == -2 and "2^30" in str(ei.value)
+    m = Mesh(3, 2048, 1, rank=0, nranks=2, device=-1)      # half the layers: accepted
+    assert m.info["n_elem_local"] == 6 * 2048 ** 2 * 1024
+    m.close()
 
 
 def test_slab_error_and_operator_on_host_mesh():
