@@ -55,10 +55,13 @@ __global__ void quad_coef_kernel(WeightsArgs a, int64_t e0, int64_t nb) {
 //    optimal 2 wavefronts).  N = W_T: 165 (C5) -> 3 column blocks of 56 (2 % padding).
 constexpr int GBM = 64, GBN = 56, GK = 16, GPA = GBM + 4, GPB = GBN + 4;
 __device__ __forceinline__ void dmma_884(double& c0, double& c1, double a, double b) {
-    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
-__global__ void __launch_bounds__(128) gemm_kernel(const double* __restrict__ AT, const double* __restrict__ B,
+#ifndef DOGIP_GEMM_MINB
+#define DOGIP_GEMM_MINB 1
+#endif
+__global__ void __launch_bounds__(128, DOGIP_GEMM_MINB) gemm_kernel(const double* __restrict__ AT, const double* __restrict__ B,
                                                    double* __restrict__ C, int64_t M, int N, int K) {
     __shared__ __align__(16) double As[GK][GPA];
     __shared__ __align__(16) double Bs[GK][GPB];
@@ -134,6 +137,7 @@ __global__ void __launch_bounds__(128) gemm_kernel(const double* __restrict__ AT
                 if (gm < M && gn < N) C[(int64_t)gn * M + gm] = acc[mt][nt][h];   // C^T: [n][m]
             }
 }
+
 
 // 3. congruence + tile-major store.  direct: cell-constant coefficient.
 template <int D>
