@@ -28,7 +28,7 @@
  *    dogip_apply calls on one op may run concurrently on different streams
  *    with distinct y.  Calls that use library-owned scratch are
  *    NOT re-entrant per handle: dogip_apply_host and dogip_cg (per op), and
- *    any call that exchanges interface planes (nranks > 1, per mesh) --
+ *    any call that exchanges interface planes (mesh with a communicator) --
  *    serialise those on one stream / thread per handle.
  *  - Multi-GPU (nranks > 1): one process per GPU; every call is collective and
  *    must be made by all ranks in the same order.  The mesh is split into
@@ -175,14 +175,17 @@ const char* dogip_last_error(void);
 
 /*
  * dogip_mesh_setup -- structured mesh M_N, P_p DoF plan and
- * slab partition; with nranks > 1 also the NCCL communicator.
+ * slab partition; with nccl_id also the NCCL communicator.
  *   d, N, p     dimension (2|3), cells per axis (>= 1, >= nranks), order (1..4)
  *   vertices    host array ((N+1)^d, d) of vertex coordinates in vertex order,
  *               or NULL for the lattice {0,1/N,..,1}^d (copied; caller keeps it)
  *   rank/nranks this process and the world size (0/1 for one GPU)
  *   nccl_id     128-byte ncclUniqueId created by rank 0 and broadcast by the
- *               caller (torch.distributed), NULL when nranks == 1 or when the
- *               caller only wants partial sums (DOGIP_NO_EXCHANGE)
+ *               caller (torch.distributed); NULL when the caller only wants partial
+ *               sums (DOGIP_NO_EXCHANGE) or runs one rank without NCCL.  Any non-NULL
+ *               id (also with nranks = 1) creates the communicator, and every apply /
+ *               load vector / CG then runs the exchange and all-reduce path (a 1-rank
+ *               communicator makes them identities: a single-GPU check of the plumbing)
  *   device      CUDA device ordinal used by every later call on this mesh; -1 builds a
  *               host-only mesh (info / dofmap introspection, no device work)
  * Errors: E_INVALID_DIM, E_INVALID_SIZE, E_UNSUPPORTED_ORDER,

@@ -197,7 +197,7 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
         if (e == cudaSuccess) e = cudaMemcpy(m->d_verts, vertices, sizeof(double) * nv * d, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) { cudaFree(m->d_verts); delete m; return fail(DOGIP_E_OOM, "vertex upload failed"); }
     }
-    if (nranks > 1 && nccl_id) {
+    if (nccl_id) {   // also for nranks = 1: exercises the exchange / all-reduce plumbing
         auto& api = nccl();
         if (!api.ok) { dogip_mesh_destroy(m); return fail(DOGIP_E_NCCL, api.err); }
         ncclUniqueId id;
@@ -524,7 +524,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         op->d_w = wg;
         op->w_doubles = m->geo.ndof_w;
         if (ce != cudaSuccess) { cudaFree(cnt); return cleanup_fail(DOGIP_E_CUDA, std::string("globalize: ") + cudaGetErrorString(ce)); }
-        if (m->nranks > 1 && m->comm) {
+        if (m->comm) {
             const int64_t PW = m->d == 3 ? MW * MW : MW;
             int rc = sum_interface_planes(m, wg, PW, m->geo.ndof_w, st);
             if (rc >= 0) rc = sum_interface_planes(m, cnt, PW, m->geo.ndof_w, st);
@@ -647,7 +647,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
         if (op->store == DOGIP_STORE_QP) return launch_qp_apply(qp_args(op, a));
         return launch_apply(a);
     };
-    const bool xchg = m->nranks > 1 && m->comm && !(flags & DOGIP_NO_EXCHANGE);
+    const bool xchg = m->comm && !(flags & DOGIP_NO_EXCHANGE);
     if (!xchg) {
         CK(launch(0, g.ntiles));
     } else {
@@ -767,7 +767,7 @@ extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_hos
         CK(cudaMalloc(&op->hu, sizeof(double) * n));
         CK(cudaMalloc(&op->hy, sizeof(double) * n));
     }
-    const bool xchg = op->m->nranks > 1 && op->m->comm && !(flags & DOGIP_NO_EXCHANGE);
+    const bool xchg = op->m->comm && !(flags & DOGIP_NO_EXCHANGE);
     if (!xchg) return apply_host_pipelined(op, u_host, y_host, flags, st);
     CK(cudaMemcpyAsync(op->hu, u_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     RET(dogip_apply(op, op->hu, op->hy, flags, stream));
@@ -782,7 +782,7 @@ extern "C" int dogip_load_vector(dogip_op op, double f, double* b, unsigned flag
     dogip_mesh_s* m = op->m;
     CK(cudaMemsetAsync(b, 0, sizeof(double) * m->geo.ndof, st));
     CK(launch_load_vector(m->geo, m->p, m->d_verts, op->d_sV, op->ref.VT, &m->tab, f, b, st));
-    if (m->nranks > 1 && m->comm && !(flags & DOGIP_NO_EXCHANGE)) {
+    if (m->comm && !(flags & DOGIP_NO_EXCHANGE)) {
         CK(cudaEventRecord(m->ev_bnd, st));
         RET(exchange_planes(m, b, m->ev_bnd));
         RET(finish_exchange(m, b, st));
@@ -793,7 +793,7 @@ extern "C" int dogip_load_vector(dogip_op op, double f, double* b, unsigned flag
 
 // ------------------------------------------------------------------ CG
 static int allreduce_scalar(dogip_mesh_s* m, double* s, cudaStream_t st) {
-    if (m->nranks > 1 && m->comm) NK(nccl().AllReduce(s, s, 1, ncclDouble, ncclSum, m->comm, st));
+    if (m->comm) NK(nccl().AllReduce(s, s, 1, ncclDouble, ncclSum, m->comm, st));
     return DOGIP_OK;
 }
 
@@ -897,7 +897,7 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
         for (auto& e : aev) CK(cudaEventCreate(&e));
     }
     // the graph-captured loop is built (or reused) before the timed region
-    const bool graph_ok = !bench && nit > 0 && m->nranks == 1 && std::getenv("DOGIP_CG_NO_GRAPH") == nullptr;
+    const bool graph_ok = !bench && nit > 0 && !m->comm && std::getenv("DOGIP_CG_NO_GRAPH") == nullptr;
     if (graph_ok) RET(cg_graph_build(op, x, rtol, nit, aflags, st));
     CK(cudaEventRecord(t0, st));
     if (!resume) {

@@ -613,3 +613,39 @@ def test_sym_storage_errors():
     with pytest.raises(DogipError) as ei:
         Operator(m, 1, TANH3, storage=5)
     assert ei.value.code == -10
+
+
+# ------------------------------------------------------------------ NCCL plumbing
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,N,p,form,storage", [(3, 5, 2, 1, 0), (3, 4, 3, 0, 2), (2, 40, 2, 1, 0)])
+def test_nccl_single_rank_communicator(d, N, p, form, storage):
+    """A mesh created with an NCCL id runs the multi-GPU code path -- communicator init
+    (dlopen'd NCCL), boundary layers first, grouped send/recv on the comm stream, plane
+    add, all-reduced CG dots, host-loop CG, exchange-path host apply -- which with a
+    1-rank communicator must reproduce the plain single-GPU results.  No rank waits on
+    another (one process, one GPU)."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator, nccl_unique_id
+    coef = Coefficient(COEF_CONST, np.array([1.3]))
+    m0 = Mesh(d, N, p, device=0)
+    m1 = Mesh(d, N, p, nranks=1, nccl_id=nccl_unique_id(), device=0)
+    op0 = Operator(m0, form, coef, storage=storage)
+    op1 = Operator(m1, form, coef, storage=storage)
+    u = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, m0.ndof)).cuda()
+    for dirichlet in (False, True):
+        y0 = op0.apply(u, dirichlet=dirichlet)
+        y1 = op1.apply(u, dirichlet=dirichlet)
+        torch.cuda.synchronize()
+        assert relerr(y1.cpu().numpy(), y0.cpu().numpy()) <= 1e-13
+    h1 = op1.apply_host(u.cpu().numpy(), dirichlet=True)
+    assert relerr(h1, op0.apply(u, dirichlet=True).cpu().numpy()) <= 1e-13
+    dirichlet = form == 1
+    b0 = op0.load_vector(1.0, dirichlet=dirichlet)
+    b1 = op1.load_vector(1.0, dirichlet=dirichlet)
+    assert relerr(b1.cpu().numpy(), b0.cpu().numpy()) <= 1e-14
+    x0, x1 = torch.zeros_like(b0), torch.zeros_like(b1)
+    r0 = op0.cg(b0, x0, rtol=1e-10, dirichlet=dirichlet)
+    r1 = op1.cg(b1, x1, rtol=1e-10, dirichlet=dirichlet)
+    assert r0["status"] == r1["status"] == "OK"
+    assert abs(r0["iters"] - r1["iters"]) <= 2
+    assert relerr(x1.cpu().numpy(), x0.cpu().numpy()) <= 1e-8
