@@ -86,19 +86,22 @@ static int emit_combo(FILE* f, const char* indent, const std::string& dst, bool 
 // interpolated values per emission group (argv[2]); 1 = node by node, which measured
 // best on B200 (profiles/r01_ab_variants.log: grouping 12 values was neutral-to-worse)
 static int g_gmax_vals = 1;
-// EL bodies through the barycentric derivatives (argv[6]; default 0 = off): per node
+// EL bodies through the barycentric derivatives (argv[6]: bit 0 interpolation, bit 1
+// projection (3D; bit 2 also 2D); default 2): per node
 //   t_i = sum_l D_i[j,l] u_l (i = 0..d),  g_r = t_{r+1} - t_0,
 //   y_l += sum_{i>=1} D_i[j,l] h_{i-1} - D_0[j,l] (h_0 + .. + h_{d-1})
 // = the Bhat_EL body exactly (Bhat_r = D_{r+1} - D_0), with 3D P3 740 instead of 1014
 // table nonzeros per direction (tables.hpp bary_deriv_table).
-static int g_bary = 0;   // measured slower on B200 (spills; profiles/r01_ab_bary_deriv.log)
+static int g_bary = 2;   // default: projection only, 3D only (profiles/r01_ab_bary_deriv.log:
+                         // the interpolation half spills at 168 registers; 2D measured 1-2 % slower)
 
 static void emit_variant(FILE* f, int d, int p, int form, int store) {
     Table t = bhat_table(d, p, form);
     const int VT = t.cols, WT = t.rows;
-    const bool bary = form == 1 && g_bary;
+    const bool bary = form == 1 && (g_bary & 1), bary_p = form == 1 && (g_bary & 2) && (d == 3 || (g_bary & 4));
+    const bool bary_any = bary || bary_p;
     Table D;
-    if (bary) D = bary_deriv_table(d, p);
+    if (bary_any) D = bary_deriv_table(d, p);
     const int NSYM = d * (d + 1) / 2;
     const int NC = (form == 0 || store == 1) ? 1 : NSYM;
     const int NG = store == 1 ? NSYM : 0;
@@ -216,7 +219,7 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
                     flops += 2 * d - 1;
                 }
             }
-            if (bary) {
+            if (bary_p) {
                 bool d0 = false;
                 for (int l = 0; l < VT; ++l) d0 |= !D.at(0, j, l).is_zero();
                 if (d0) {
