@@ -82,7 +82,8 @@ extern "C" {
                                 gathered per element; multi-rank needs the NCCL communicator */
 #define DOGIP_STORE_PAIR   3 /* WP only: the values of DOGIP_STORE_FULL in the paired-lane layout
                                 (two lanes per element, node pairs (j, sigma j) in adjacent rows of
-                                16-element half-tiles); same bytes, fewer registers per lane */
+                                16-element half-tiles); same bytes, fewer registers per lane;
+                                no Dirichlet elimination (DOGIP_DIRICHLET_ZERO -> E_INVALID_ARG) */
 #define DOGIP_STORE_SYM    5 /* WP only: the same weights in symmetry-adapted form -- per orbit P of
                                 the double-grid nodes under the barycentric involutions
                                 G = <(0 1), (2 3)> (3D) / <(0 1)> (2D), ahat_psi(P) = (1/|G|) sum_g

@@ -618,6 +618,13 @@ static QpArgs qp_args(dogip_op op, const ApplyArgs& a) {
     return q;
 }
 
+// The paired-lane WP kernel (DOGIP_STORE_PAIR) has no boundary masks.
+static int check_dirichlet_storage(dogip_op op, unsigned flags) {
+    if ((flags & DOGIP_DIRICHLET_ZERO) && op->store == DOGIP_STORE_PAIR)
+        return fail(DOGIP_E_INVALID_ARG, "DOGIP_DIRICHLET_ZERO is not supported with DOGIP_STORE_PAIR");
+    return DOGIP_OK;
+}
+
 // y = A u (+ exchange); with dot != null also *dot = u^T y over this rank's elements
 // (+ boundary rows owned by this rank), fused into the apply kernel (CG's p.q).
 static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, cudaStream_t st,
@@ -688,6 +695,7 @@ extern "C" int dogip_apply(dogip_op op, const double* u, double* y, unsigned fla
     if (!op || !u || !y) return fail(DOGIP_E_INVALID_ARG, "null argument");
     if (u == y) return fail(DOGIP_E_INVALID_ARG, "u and y must not alias");
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
+    RET(check_dirichlet_storage(op, flags));
     return apply_impl(op, u, y, flags, (cudaStream_t)stream);
 }
 
@@ -760,6 +768,7 @@ static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_hos
 extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_host, unsigned flags, void* stream) {
     if (!op || !u_host || !y_host) return fail(DOGIP_E_INVALID_ARG, "null argument");
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
+    RET(check_dirichlet_storage(op, flags));
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = op->m->geo.ndof;
     CK(cudaSetDevice(op->m->device));
@@ -863,6 +872,7 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
                         void* stream, dogip_cg_result* res) {
     if (!op || !b || !x || !res) return fail(DOGIP_E_INVALID_ARG, "null argument");
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_CG_RESUME)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
+    RET(check_dirichlet_storage(op, flags));
     cudaStream_t st = (cudaStream_t)stream;
     dogip_mesh_s* m = op->m;
     const int64_t n = m->geo.ndof;

@@ -700,9 +700,12 @@ cudaError_t launch_dir(const ApplyArgs& a) {
 
 template <int D, int P>
 cudaError_t launch_form(const ApplyArgs& a) {
-    if (a.form == 0 && a.store == 2) return launch_one<D, P, 0, 0, false, true>(a);   // WP has no BC
+    // Dirichlet elimination (DOGIP_DIRICHLET_ZERO) for every storage but PAIR, whose
+    // paired-lane kernel has no boundary masks (abi.cu rejects that combination)
+    if (a.form == 0 && a.store == 2)
+        return a.dirichlet ? launch_one<D, P, 0, 0, true, true>(a) : launch_one<D, P, 0, 0, false, true>(a);
     if (a.form == 0 && a.store == 3) return launch_pair<D, P>(a);
-    if (a.form == 0 && a.store == 5) return launch_one<D, P, 0, 5, false, false>(a);
+    if (a.form == 0 && a.store == 5) return launch_dir<D, P, 0, 5>(a);
     if (a.form == 0) return launch_dir<D, P, 0, 0>(a);
     return a.store == 1 ? launch_dir<D, P, 1, 1>(a) : launch_dir<D, P, 1, 0>(a);
 }

@@ -334,7 +334,8 @@ cudaError_t launch_qp_one(const QpArgs& a) {
 
 template <int D, int P, bool CC>
 cudaError_t launch_qp_dpc(const QpArgs& a) {
-    if (a.form == 0) return launch_qp_one<D, P, 0, false, CC>(a);
+    if (a.form == 0)
+        return a.dirichlet ? launch_qp_one<D, P, 0, true, CC>(a) : launch_qp_one<D, P, 0, false, CC>(a);
     return a.dirichlet ? launch_qp_one<D, P, 1, true, CC>(a) : launch_qp_one<D, P, 1, false, CC>(a);
 }
 

@@ -649,3 +649,44 @@ def test_nccl_single_rank_communicator(d, N, p, form, storage):
     assert r0["status"] == r1["status"] == "OK"
     assert abs(r0["iters"] - r1["iters"]) <= 2
     assert relerr(x1.cpu().numpy(), x0.cpu().numpy()) <= 1e-8
+
+
+# ------------------------------------------------------------------ degenerate sizes
+STORES_BY_FORM = {0: (0, 2, 3, 4, 5), 1: (0, 1, 4)}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,p,form", ALL)
+@pytest.mark.parametrize("N", [1, 2])
+def test_smallest_meshes_every_storage(d, p, form, N):
+    """N = 1 (one cell: one tile with 1 live lane of 32) and N = 2, every storage variant,
+    against the assembled oracle A; with Dirichlet elimination the boundary rows are
+    identity rows (at N = 1, p <= 2 every DoF is on the boundary, so A_D = I) and CG on
+    b = 0 returns x = 0 at once."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    coef = coef_for(d, form, "tanh") if form == 0 else Coefficient(COEF_CONST, np.array([1.7]))
+    ed = oa.build(d, N, p)
+    A = oa.assemble_csr(ed, form, coef)
+    mask = boundary_mask(d, N, p)
+    AD = oa.dirichlet_matrix(A, mask)
+    u = u_vector(ed.ndof, 1)
+    m = Mesh(d, N, p, device=0)
+    ut = torch.from_numpy(u).cuda()
+    for store in STORES_BY_FORM[form]:
+        op = Operator(m, form, coef, storage=store)
+        y = op.apply(ut).cpu().numpy()
+        assert relerr(y, A @ u) <= TOL, store
+        if store == 3:       # the paired-lane layout has no Dirichlet elimination
+            with pytest.raises(RuntimeError, match="PAIR"):
+                op.apply(ut, dirichlet=True)
+            op.close()
+            continue
+        yd = op.apply(ut, dirichlet=True).cpu().numpy()
+        assert relerr(yd, AD @ u) <= TOL, store
+        b = torch.zeros_like(ut)
+        x = torch.zeros_like(ut)
+        r = op.cg(b, x, rtol=1e-10, dirichlet=True)
+        assert r["status"] == "OK" and r["iters"] == 0 and not x.abs().max().item()
+        op.close()
+    m.close()
