@@ -690,3 +690,48 @@ def test_smallest_meshes_every_storage(d, p, form, N):
         assert r["status"] == "OK" and r["iters"] == 0 and not x.abs().max().item()
         op.close()
     m.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,p,form", ALL)
+def test_every_storage_every_entry_point(d, p, form):
+    """Cross product on a jittered mesh with a ragged x-block: every storage of the form x
+    {device apply, host-buffer apply} x {plain, Dirichlet-eliminated} against the oracle's
+    A / A_D, and 6 fixed-count CG iterations from x0 = 0 (graph and host loop) against the
+    oracle's CG run for the same count."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    N = 34 if d == 2 else 3
+    verts = jitter_verts(d, N)
+    coef = coef_for(d, form, "tanh") if form == 0 else Coefficient(COEF_CONST, np.array([0.8]))
+    ed = oa.build(d, N, p, verts)
+    A = oa.assemble_csr(ed, form, coef)
+    AD = oa.dirichlet_matrix(A, boundary_mask(d, N, p))
+    u = u_vector(ed.ndof, 2)
+    b = oa.load_vector(ed, 1.0, dirichlet=True)
+    x_ref6, _, _, _ = oracle_cg(lambda v: AD @ v, b, rtol=0.0, maxit=6)
+    m = Mesh(d, N, p, verts, device=0)
+    ut = torch.from_numpy(u).cuda()
+    for store in STORES_BY_FORM[form]:
+        op = Operator(m, form, coef, storage=store)
+        dirs = (False,) if store == 3 else (False, True)
+        for dirichlet in dirs:
+            ref = (AD if dirichlet else A) @ u
+            assert relerr(op.apply(ut, dirichlet=dirichlet).cpu().numpy(), ref) <= TOL, (store, dirichlet)
+            assert relerr(op.apply_host(u, dirichlet=dirichlet), ref) <= TOL, (store, dirichlet, "host")
+        if store != 3:
+            bt = torch.from_numpy(b).cuda()
+            for graph in (True, False):
+                x = torch.zeros_like(bt)
+                if not graph:
+                    import os
+                    os.environ["DOGIP_CG_NO_GRAPH"] = "1"
+                try:
+                    r = op.cg(bt, x, rtol=1e-300, maxit=6, dirichlet=True)
+                finally:
+                    if not graph:
+                        del os.environ["DOGIP_CG_NO_GRAPH"]
+                assert r["iters"] == 6
+                assert relerr(x.cpu().numpy(), x_ref6) <= 1e-9, (store, graph)
+        op.close()
+    m.close()
