@@ -735,3 +735,48 @@ def test_every_storage_every_entry_point(d, p, form):
                 assert relerr(x.cpu().numpy(), x_ref6) <= 1e-9, (store, graph)
         op.close()
     m.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,N,p,form,nr", [(3, 6, 2, 1, 2), (3, 5, 4, 0, 3), (2, 40, 3, 0, 2), (2, 36, 2, 1, 3)])
+def test_slab_partials_every_storage(d, N, p, form, nr):
+    """Slab partials (DOGIP_NO_EXCHANGE, no communicator) summed over ranks equal the
+    single-rank apply for every storage that runs without a communicator (GLOBAL needs
+    one on several ranks and is rejected without it), with and without Dirichlet."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    from paper_1710_09913_b200._lib import DogipError
+    coef = coef_for(d, form, "tanh") if form == 0 else Coefficient(COEF_CONST, np.array([1.1]))
+    verts = jitter_verts(d, N)
+    Md = p * N + 1
+    u = u_vector(Md ** d, 6)
+    mg = Mesh(d, N, p, verts, device=0)
+    ug = torch.from_numpy(u).cuda()
+    meshes = [Mesh(d, N, p, verts, rank=r, nranks=nr, device=0) for r in range(nr)]
+    for store in STORES_BY_FORM[form]:
+        if store == 2:
+            with pytest.raises(DogipError):
+                Operator(meshes[0], form, coef, storage=store)
+            continue
+        opg = Operator(mg, form, coef, storage=store)
+        ops = [Operator(m, form, coef, storage=store) for m in meshes]
+        for dirichlet in ((False,) if store == 3 else (False, True)):
+            y_glob = opg.apply(ug, dirichlet=dirichlet).cpu().numpy()
+            acc = np.zeros_like(u)
+            for m, op in zip(meshes, ops):
+                i0 = m.info["dof_offset"]
+                ul = torch.from_numpy(u[i0:i0 + m.ndof].copy()).cuda()
+                acc[i0:i0 + m.ndof] += op.apply(ul, exchange=False, dirichlet=dirichlet).cpu().numpy()
+            if dirichlet:
+                # interface planes hold Dirichlet rows (u_i) on both owners: count them once
+                mask = boundary_mask(d, N, p)
+                plane = Md ** (d - 1)
+                for r in range(1, nr):
+                    i0 = meshes[r].info["dof_offset"]
+                    sl = slice(i0, i0 + plane)
+                    acc[sl][mask[sl]] -= u[sl][mask[sl]]
+            assert relerr(acc, y_glob) <= 1e-13, (store, dirichlet)
+        for op in ops + [opg]:
+            op.close()
+    for m in meshes + [mg]:
+        m.close()
