@@ -780,3 +780,47 @@ def test_slab_partials_every_storage(d, N, p, form, nr):
             op.close()
     for m in meshes + [mg]:
         m.close()
+
+
+def _coef_kinds(d, form, N):
+    out = [("const", Coefficient(COEF_CONST, np.array([1.4]))),
+           ("per_cell", Coefficient(COEF_PER_CELL, np.zeros(0), grf_per_cell(d, N, 0.2, 1.0, 3))),
+           ("tanh", TANH2 if d == 2 else TANH3)]
+    if d == 2:
+        out.append(("sincos", SINCOS))
+    if form == 1:
+        T = np.array([[2.0, 0.3], [0.3, 1.0]]) if d == 2 else np.array([[2.0, 0.3, 0.1], [0.3, 1.0, -0.2],
+                                                                          [0.1, -0.2, 1.5]])
+        out.append(("tensor", Coefficient(COEF_CONST_TENSOR, T.ravel())))
+        if d == 3:
+            out.append(("aniso", ANISO))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,p,form", [(2, 2, 0), (2, 3, 1), (3, 2, 0), (3, 2, 1), (3, 3, 1), (3, 4, 0)])
+def test_every_coefficient_kind_every_storage(d, p, form):
+    """Every coefficient model valid for (d, form) x every storage that accepts it, on a
+    jittered mesh, against the oracle's assembled A (the same rule, reading L10); storages
+    that need an isotropic coefficient reject the tensor kinds with E_BAD_COEFF."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    from paper_1710_09913_b200._lib import DogipError
+    N = 34 if d == 2 else 3
+    verts = jitter_verts(d, N)
+    ed = oa.build(d, N, p, verts)
+    u = u_vector(ed.ndof, 4)
+    m = Mesh(d, N, p, verts, device=0)
+    ut = torch.from_numpy(u).cuda()
+    for name, coef in _coef_kinds(d, form, N):
+        A = oa.assemble_csr(ed, form, coef)
+        for store in STORES_BY_FORM[form]:
+            if store == 1 and not coef.isotropic:
+                with pytest.raises(DogipError) as ei:
+                    Operator(m, form, coef, storage=store)
+                assert ei.value.code == -5
+                continue
+            op = Operator(m, form, coef, storage=store)
+            assert relerr(op.apply(ut).cpu().numpy(), A @ u) <= TOL, (name, store)
+            op.close()
+    m.close()
