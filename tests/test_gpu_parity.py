@@ -824,3 +824,65 @@ def test_every_coefficient_kind_every_storage(d, p, form):
             assert relerr(op.apply(ut).cpu().numpy(), A @ u) <= TOL, (name, store)
             op.close()
     m.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n1d", [2, 5, 9])
+def test_quadrature_order_every_storage(n1d):
+    """A non-default rule (quad_n1d) reaches the weights kernels and the comparator alike:
+    every WP storage and the EL storages equal the oracle assembled with the same rule."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    d, N, p = 3, 3, 3
+    verts = jitter_verts(d, N)
+    ed = oa.build(d, N, p, verts, n1d=n1d)
+    u = u_vector(ed.ndof, 8)
+    m = Mesh(d, N, p, verts, device=0)
+    ut = torch.from_numpy(u).cuda()
+    for form, coef in ((0, TANH3), (1, Coefficient(COEF_TANH_RADIAL, TANH3.params))):
+        A = oa.assemble_csr(ed, form, coef)
+        for store in STORES_BY_FORM[form]:
+            op = Operator(m, form, coef, quad_n1d=n1d, storage=store)
+            assert relerr(op.apply(ut).cpu().numpy(), A @ u) <= TOL, (form, store)
+            op.close()
+    m.close()
+
+
+@pytest.mark.gpu
+def test_user_streams_and_concurrent_applies():
+    """Work on caller streams (apply, host apply, CG graph) and two concurrent applies of
+    one op on two streams into distinct y (dogip.h concurrency note)."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    d, N, p, form = 3, 6, 3, 1
+    coef = Coefficient(COEF_CONST, np.array([1.2]))
+    ed = oa.build(d, N, p)
+    A = oa.assemble_csr(ed, form, coef)
+    AD = oa.dirichlet_matrix(A, boundary_mask(d, N, p))
+    u = u_vector(ed.ndof, 9)
+    m = Mesh(d, N, p, device=0)
+    op = Operator(m, form, coef)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ut = torch.from_numpy(u).cuda()
+    torch.cuda.synchronize()
+    y1, y2 = torch.empty_like(ut), torch.empty_like(ut)
+    for _ in range(5):
+        with torch.cuda.stream(s1):
+            op.apply(ut, y1, stream=s1)
+        with torch.cuda.stream(s2):
+            op.apply(ut, y2, dirichlet=True, stream=s2)
+    torch.cuda.synchronize()
+    assert relerr(y1.cpu().numpy(), A @ u) <= TOL
+    assert relerr(y2.cpu().numpy(), AD @ u) <= TOL
+    with torch.cuda.stream(s1):
+        b = op.load_vector(1.0, dirichlet=True, stream=s1)
+        x = torch.zeros_like(b)
+        r = op.cg(b, x, rtol=1e-10, dirichlet=True, stream=s1)
+    torch.cuda.synchronize()
+    bn = b.cpu().numpy()
+    assert r["status"] == "OK"
+    assert np.linalg.norm(AD @ x.cpu().numpy() - bn) <= 2e-10 * np.linalg.norm(bn)
+    hy = op.apply_host(u, dirichlet=True, stream=s2)
+    assert relerr(hy, AD @ u) <= TOL
+    op.close()
+    m.close()
