@@ -617,7 +617,8 @@ def test_sym_storage_errors():
 
 # ------------------------------------------------------------------ NCCL plumbing
 @pytest.mark.gpu
-@pytest.mark.parametrize("d,N,p,form,storage", [(3, 5, 2, 1, 0), (3, 4, 3, 0, 2), (2, 40, 2, 1, 0)])
+@pytest.mark.parametrize("d,N,p,form,storage", [(3, 5, 2, 1, 0), (3, 4, 3, 0, 2), (2, 40, 2, 1, 0), (3, 4, 4, 0, 5),
+                                                (3, 4, 3, 1, 4), (3, 5, 3, 1, 1), (2, 40, 3, 0, 0)])
 def test_nccl_single_rank_communicator(d, N, p, form, storage):
     """A mesh created with an NCCL id runs the multi-GPU code path -- communicator init
     (dlopen'd NCCL), boundary layers first, grouped send/recv on the comm stream, plane
