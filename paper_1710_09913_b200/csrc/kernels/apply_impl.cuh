@@ -34,6 +34,9 @@
 #include "apply.cuh"
 #include "common.cuh"
 
+#ifndef DOGIP_ISO_STAGES
+#define DOGIP_ISO_STAGES 2      // ring stages of the ISO kernels (0 = DOGIP_STAGES)
+#endif
 #ifndef DOGIP_LOCKSTEP
 #define DOGIP_LOCKSTEP -1      // CTA barrier at every weight chunk (the CTA's warps share I-cache
                                // lines): -1 per-variant policy, 0 never, 1 always (A/B builds)
@@ -103,10 +106,12 @@ struct Chunking {
     // ring stages per (d, p, form, storage), from the B200 A/B of 2/3/4 stages
     // (profiles/r01_ab_ring_stages.log): double buffering wins for the long weight tiles of
     // 3D P3 EL (C4: 3.72 -> 3.45 ms), 2D P4 EL and the symmetry-adapted kernel, 4 stages
-    // for the rest (C2 p=2, C3, C4 iso, C5 full lose 1-6 % with 2)
+    // for the rest (C2 p=2, C3, C5 full lose 1-6 % with 2).  The ISO kernels (NG > 0) run
+    // CTA-lockstepped and take 2 (C4 iso 2.17 -> 2.13 ms, r01_ab_bary_deriv.log tail)
     static constexpr int S = DOGIP_STAGES_FORCE > 0 ? DOGIP_STAGES_FORCE
                            : RE::DOT_IN_BODY ? DOGIP_SYM_STAGES
                            : (RE::NC > 1 && RE::TILE_ROWS >= 84) ? 2
+                           : (RE::NG > 0 && DOGIP_ISO_STAGES > 0) ? DOGIP_ISO_STAGES
                            : DOGIP_STAGES;
     static constexpr int TILE_ROWS = RE::TILE_ROWS;
     static constexpr int AL = RE::RALIGN;                                  // chunk boundaries fall on rows % AL == 0
