@@ -35,12 +35,14 @@ def _stream_ptr(stream) -> Optional[int]:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def _tensor_ptr(t, n: int) -> int:
+def _tensor_ptr(t, n: int, device: Optional[int] = None) -> int:
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise TypeError("expected a contiguous float64 CUDA tensor")
     if t.numel() != n:
         raise ValueError(f"expected {n} entries, got {t.numel()}")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"tensor on cuda:{t.device.index}, mesh on cuda:{device}")
     return t.data_ptr()
 
 
@@ -151,14 +153,21 @@ class Operator:
         self.form = form
 
     # -- apply ---------------------------------------------------------------
+    def _device(self):
+        """The mesh's CUDA device made current for a call (the C ABI launches on the
+        caller's current device / stream)."""
+        import torch
+        return torch.cuda.device(self.mesh.device)
+
     def apply(self, u, y=None, dirichlet: bool = False, exchange: bool = True, stream=None):
         import torch
         if y is None:
             y = torch.empty_like(u)
         flags = (DOGIP_DIRICHLET_ZERO if dirichlet else 0) | (0 if exchange else DOGIP_NO_EXCHANGE)
-        check(self._lib.dogip_apply(self.handle, C.c_void_p(_tensor_ptr(u, self.ndof)),
-                                    C.c_void_p(_tensor_ptr(y, self.ndof)), flags,
-                                    C.c_void_p(_stream_ptr(stream))))
+        with self._device():
+            check(self._lib.dogip_apply(self.handle, C.c_void_p(_tensor_ptr(u, self.ndof, self.mesh.device)),
+                                        C.c_void_p(_tensor_ptr(y, self.ndof, self.mesh.device)), flags,
+                                        C.c_void_p(_stream_ptr(stream))))
         return y
 
     def apply_host(self, u: np.ndarray, y: Optional[np.ndarray] = None, dirichlet: bool = False, stream=None):
@@ -167,24 +176,30 @@ class Operator:
             raise ValueError("size mismatch")
         if y is None:
             y = np.empty_like(u)
+        if not (isinstance(y, np.ndarray) and y.dtype == np.float64 and y.flags.c_contiguous and y.size == self.ndof):
+            raise TypeError(f"y must be a contiguous float64 array of {self.ndof} entries")
         flags = DOGIP_DIRICHLET_ZERO if dirichlet else 0
-        check(self._lib.dogip_apply_host(self.handle, u.ctypes.data, y.ctypes.data, flags,
-                                         C.c_void_p(_stream_ptr(stream))))
+        with self._device():
+            check(self._lib.dogip_apply_host(self.handle, u.ctypes.data, y.ctypes.data, flags,
+                                             C.c_void_p(_stream_ptr(stream))))
         return y
 
     def apply_host_ptr(self, u_ptr: int, y_ptr: int, dirichlet: bool = False, stream=None):
         """Host-buffer apply on raw (pinned) host pointers."""
         flags = DOGIP_DIRICHLET_ZERO if dirichlet else 0
-        check(self._lib.dogip_apply_host(self.handle, C.c_void_p(u_ptr), C.c_void_p(y_ptr), flags,
-                                         C.c_void_p(_stream_ptr(stream))))
+        with self._device():
+            check(self._lib.dogip_apply_host(self.handle, C.c_void_p(u_ptr), C.c_void_p(y_ptr), flags,
+                                             C.c_void_p(_stream_ptr(stream))))
 
     def load_vector(self, f: float = 1.0, dirichlet: bool = False, out=None, stream=None):
         import torch
         if out is None:
             out = torch.empty(self.ndof, dtype=torch.float64, device=f"cuda:{self.mesh.device}")
         flags = DOGIP_DIRICHLET_ZERO if dirichlet else 0
-        check(self._lib.dogip_load_vector(self.handle, float(f), C.c_void_p(_tensor_ptr(out, self.ndof)), flags,
-                                          C.c_void_p(_stream_ptr(stream))))
+        with self._device():
+            check(self._lib.dogip_load_vector(self.handle, float(f),
+                                              C.c_void_p(_tensor_ptr(out, self.ndof, self.mesh.device)), flags,
+                                              C.c_void_p(_stream_ptr(stream))))
         return out
 
     def cg(self, b, x, rtol: float = 1e-10, maxit: int = 10000, dirichlet: bool = False, stream=None,
@@ -193,9 +208,10 @@ class Operator:
         (benchmarking); resume: continue the previous call's iteration."""
         res = _lib.CgResult()
         flags = (DOGIP_DIRICHLET_ZERO if dirichlet else 0) | (_lib.DOGIP_CG_RESUME if resume else 0)
-        rc = self._lib.dogip_cg(self.handle, C.c_void_p(_tensor_ptr(b, self.ndof)),
-                                C.c_void_p(_tensor_ptr(x, self.ndof)), float(rtol), int(maxit), flags,
-                                C.c_void_p(_stream_ptr(stream)), C.byref(res))
+        with self._device():
+            rc = self._lib.dogip_cg(self.handle, C.c_void_p(_tensor_ptr(b, self.ndof, self.mesh.device)),
+                                    C.c_void_p(_tensor_ptr(x, self.ndof, self.mesh.device)), float(rtol), int(maxit),
+                                    flags, C.c_void_p(_stream_ptr(stream)), C.byref(res))
         if rc < 0 and rc != -9:
             check(rc)
         return {"iters": res.iters, "status": _lib.STATUS.get(res.status, res.status),
