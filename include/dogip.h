@@ -23,7 +23,9 @@
  *    never frees them.  Handles are library-owned (destroy with *_destroy).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Work is asynchronous on that stream, except dogip_cg and the *_host
- *    entry points, which synchronise it.
+ *    entry points, which synchronise it.  dogip_apply / dogip_load_vector /
+ *    dogip_cg launch on the caller's current CUDA device, which must be the
+ *    mesh's `device` (the Python binding makes it current around each call).
  *  - Concurrency: an op is read-only after dogip_weights, so single-rank
  *    dogip_apply calls on one op may run concurrently on different streams
  *    with distinct y.  Calls that use library-owned scratch are
