@@ -50,6 +50,9 @@
 #ifndef DOGIP_ROWS_3CTA
 #define DOGIP_ROWS_3CTA 18      // max rows per chunk when 3 CTAs share an SM
 #endif
+#ifndef DOGIP_ROWS_3CTA_2D
+#define DOGIP_ROWS_3CTA_2D 24   // 2D full-storage kernels at 3 CTAs: fewer, larger chunks (C2 p=3/4 -1-2 %)
+#endif
 #ifndef DOGIP_ROWS_2CTA
 #define DOGIP_ROWS_2CTA 24      // ... when 2 CTAs share an SM
 #endif
@@ -117,7 +120,7 @@ struct Chunking {
     static constexpr int AL = RE::RALIGN;                                  // chunk boundaries fall on rows % AL == 0
     // the symmetry-adapted kernel stages u_T in shared memory too: 16-row chunks keep 2 CTAs/SM
     static constexpr int ROWS_MAX0 = min_blocks<RE>() >= 4 ? DOGIP_ROWS_4CTA
-                                     : min_blocks<RE>() >= 3 ? DOGIP_ROWS_3CTA
+                                     : min_blocks<RE>() >= 3 ? ((RE::NS == 2 && RE::NG == 0) ? DOGIP_ROWS_3CTA_2D : DOGIP_ROWS_3CTA)
                                      : (DOGIP_SYM_UPF && RE::DOT_IN_BODY) ? DOGIP_SYM_ROWS : DOGIP_ROWS_2CTA;
     static constexpr int ROWS_MAX = (ROWS_MAX0 / AL) * AL;
     static constexpr int NCH0 = (TILE_ROWS + ROWS_MAX - 1) / ROWS_MAX;
