@@ -887,3 +887,25 @@ def test_user_streams_and_concurrent_applies():
     assert relerr(hy, AD @ u) <= TOL
     op.close()
     m.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,p,form", [(2, 2, 0), (2, 3, 1), (3, 1, 1), (3, 2, 0), (3, 3, 1), (3, 4, 0)])
+def test_load_vector_every_storage(d, p, form):
+    """b_i = int phi_i (eq:linsys_gp P:207 / eq:linsys_se P:337) does not depend on the weight
+    storage: every storage's dogip_load_vector equals the oracle's, with and without the
+    Dirichlet zeroing."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    N = 34 if d == 2 else 3
+    verts = jitter_verts(d, N)
+    ed = oa.build(d, N, p, verts)
+    coef = coef_for(d, form, "tanh") if form == 0 else Coefficient(COEF_CONST, np.array([0.9]))
+    m = Mesh(d, N, p, verts, device=0)
+    for store in STORES_BY_FORM[form]:
+        op = Operator(m, form, coef, storage=store)
+        for dirichlet in (False, True):
+            b = op.load_vector(2.5, dirichlet=dirichlet).cpu().numpy()
+            assert relerr(b, oa.load_vector(ed, 2.5, dirichlet=dirichlet)) <= 1e-13, (store, dirichlet)
+        op.close()
+    m.close()
