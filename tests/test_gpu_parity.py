@@ -909,3 +909,36 @@ def test_load_vector_every_storage(d, p, form):
             assert relerr(b, oa.load_vector(ed, 2.5, dirichlet=dirichlet)) <= 1e-13, (store, dirichlet)
         op.close()
     m.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("store", [0, 1])
+def test_cg_resume_matches_one_call(store):
+    """DOGIP_CG_RESUME (the e2e_cg pattern of bench.py: one iteration per call, residual read
+    back each step) continues the iteration exactly: 6 resumed single-iteration calls equal
+    one 6-iteration call (to atomic-order rounding) and the oracle's 6 CG iterations;
+    resuming before any call is E_INVALID_ARG."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    from paper_1710_09913_b200._lib import DogipError
+    d, N, p, form = 3, 4, 3, 1
+    coef = Coefficient(COEF_CONST, np.array([1.3]))
+    ed = oa.build(d, N, p)
+    AD = oa.dirichlet_matrix(oa.assemble_csr(ed, form, coef), boundary_mask(d, N, p))
+    b = oa.load_vector(ed, 1.0, dirichlet=True)
+    x_ref, _, _, _ = oracle_cg(lambda v: AD @ v, b, rtol=0.0, maxit=6)
+    m = Mesh(d, N, p, device=0)
+    op = Operator(m, form, coef, storage=store)
+    bt = torch.from_numpy(b).cuda()
+    x1 = torch.zeros_like(bt)
+    with pytest.raises(DogipError) as ei:
+        op.cg(bt, x1, rtol=0.0, maxit=1, dirichlet=True, resume=True)
+    assert ei.value.code == -10
+    rels = [op.cg(bt, x1, rtol=0.0, maxit=1, dirichlet=True, resume=k > 0)["rel_res"] for k in range(6)]
+    x6 = torch.zeros_like(bt)
+    r6 = op.cg(bt, x6, rtol=0.0, maxit=6, dirichlet=True)
+    assert relerr(x1.cpu().numpy(), x6.cpu().numpy()) <= 1e-10
+    assert relerr(x1.cpu().numpy(), x_ref) <= 1e-9
+    assert abs(rels[-1] - r6["rel_res"]) <= 1e-9 * max(1.0, r6["rel_res"])
+    op.close()
+    m.close()
