@@ -942,3 +942,36 @@ def test_cg_resume_matches_one_call(store):
     assert abs(rels[-1] - r6["rel_res"]) <= 1e-9 * max(1.0, r6["rel_res"])
     op.close()
     m.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("form", [0, 1])
+def test_plain_dogip_weights_entry_point(form):
+    """dogip_weights (no storage argument, include/dogip.h) is the FULL storage of
+    dogip_weights_ex: same exported weights, same apply."""
+    import ctypes as C
+    torch = _torch()
+    from paper_1710_09913_b200 import _lib
+    from paper_1710_09913_b200.api import CoeffSpec, Mesh, Operator
+    d, N, p = 3, 3, 2
+    verts = jitter_verts(d, N)
+    coef = CoeffSpec.from_obj(coef_for(d, form, "smooth"))
+    m = Mesh(d, N, p, verts, device=0)
+    lib = _lib.load()
+    cs = _lib.Coeff(coef.kind, coef.params.ctypes.data_as(C.POINTER(C.c_double)), coef.params.size, None)
+    h = C.c_void_p()
+    _lib.check(lib.dogip_weights(m.handle, form, C.byref(cs), 0, None, C.byref(h)))
+    ref = Operator(m, form, coef, storage=0)
+    oi = ref.info
+    w = np.empty((m.info["n_elem_local"], oi["W_T"], oi["n_c"]))
+    _lib.check(lib.dogip_export_weights(h, w.ctypes.data_as(C.POINTER(C.c_double)), w.size))
+    assert np.array_equal(w, ref.export_weights())
+    u = torch.from_numpy(u_vector(m.ndof, 3)).cuda()
+    y = torch.empty_like(u)
+    _lib.check(lib.dogip_apply(h, C.c_void_p(u.data_ptr()), C.c_void_p(y.data_ptr()), 0,
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert relerr(y.cpu().numpy(), ref.apply(u).cpu().numpy()) <= 1e-14
+    lib.dogip_op_destroy(h)
+    ref.close()
+    m.close()
