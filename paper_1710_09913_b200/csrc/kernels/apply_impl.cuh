@@ -9,7 +9,10 @@
 //    simplex type s; one lane = one element;
 //  * the per-element work g = Bhat u_T, h = A_T g, y_T += Bhat^T h is the
 //    generated straight-line, sparsity- and +-1-aware FP64 code of
-//    generated/bhat_gen.cuh, node by node, so only u_T and y_T sit in registers;
+//    generated/bhat_gen.cuh, node by node, so only u_T and y_T sit in registers
+//    (3D EL: the projection goes through the barycentric-derivative tables,
+//    Bhat_r = D_{r+1} - D_0, 21 % fewer flops for P3; WP SYM storage: block-diagonal
+//    by character, see gen_bhat.cpp emit_sym);
 //  * A_T is stored tile-major [tile][W_T * NC][32] (lane fastest) and streamed
 //    by each warp through its own S-stage shared-memory ring with 1D bulk
 //    copies (cp.async.bulk, the TMA engine) that complete on mbarriers; the
