@@ -11,7 +11,7 @@
 //    generated straight-line, sparsity- and +-1-aware FP64 code of
 //    generated/bhat_gen.cuh, node by node, so only u_T and y_T sit in registers
 //    (3D EL: the projection goes through the barycentric-derivative tables,
-//    Bhat_r = D_{r+1} - D_0, 21 % fewer flops for P3; WP SYM storage: block-diagonal
+//    Bhat_r = D_{r+1} - D_0: 3D P3 3848 instead of 4296 flops; WP SYM storage: block-diagonal
 //    by character, see gen_bhat.cpp emit_sym);
 //  * A_T is stored tile-major [tile][W_T * NC][32] (lane fastest) and streamed
 //    by each warp through its own S-stage shared-memory ring with 1D bulk
