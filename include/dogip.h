@@ -19,8 +19,11 @@
  *  - fp64 everywhere.  Return value: 0 = OK, > 0 non-fatal status, < 0 error;
  *    the message of the last error of the calling thread is dogip_last_error().
  *  - Vectors passed to apply/cg/load_vector are CALLER-OWNED DEVICE pointers
- *    (e.g. torch CUDA tensors), contiguous, of length ndof_local; the library
- *    never frees them.  Handles are library-owned (destroy with *_destroy).
+ *    (e.g. torch CUDA tensors), contiguous, 16-byte aligned (the vector kernels
+ *    move fp64 pairs; a misaligned pointer returns E_INVALID_ARG), of length
+ *    ndof_local; the library never frees them.  Handles are library-owned
+ *    (destroy with *_destroy).  Setup / destroy / synchronous calls restore the
+ *    caller's current CUDA device on return.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *    Work is asynchronous on that stream, except dogip_cg and the *_host
  *    entry points, which synchronise it.  dogip_apply / dogip_load_vector /
@@ -82,10 +85,6 @@ extern "C" {
                                 as a W-lattice vector ((2pN+1)^d doubles) holding A_ii / mult_i
                                 (mult_i = elements sharing W node i, each visits it once) and
                                 gathered per element; multi-rank needs the NCCL communicator */
-#define DOGIP_STORE_PAIR   3 /* WP only: the values of DOGIP_STORE_FULL in the paired-lane layout
-                                (two lanes per element, node pairs (j, sigma j) in adjacent rows of
-                                16-element half-tiles); same bytes, fewer registers per lane;
-                                no Dirichlet elimination (DOGIP_DIRICHLET_ZERO -> E_INVALID_ARG) */
 #define DOGIP_STORE_SYM    5 /* WP only: the same weights in symmetry-adapted form -- per orbit P of
                                 the double-grid nodes under the barycentric involutions
                                 G = <(0 1), (2 3)> (3D) / <(0 1)> (2D), ahat_psi(P) = (1/|G|) sum_g
@@ -221,11 +220,11 @@ int dogip_weights(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_
 
 /* dogip_weights with an explicit storage variant (DOGIP_STORE_*).  DOGIP_STORE_ISO
  * needs form = DOGIP_EL (else E_INVALID_ARG) and an isotropic coefficient kind
- * (else E_BAD_COEFF); DOGIP_STORE_GLOBAL, _PAIR and _SYM need form = DOGIP_WP (else
+ * (else E_BAD_COEFF); DOGIP_STORE_GLOBAL and _SYM need form = DOGIP_WP (else
  * E_INVALID_ARG); DOGIP_STORE_QP takes both forms and stores no weights.  The apply
  * result is the same operator up to rounding for every storage.
- * dogip_export_weights returns a_{T,j} / A_{T,j} in canonical order for FULL, ISO,
- * PAIR and SYM (converted back from the stored layout), per element the stored values
+ * dogip_export_weights returns a_{T,j} / A_{T,j} in canonical order for FULL, ISO
+ * and SYM (converted back from the stored layout), per element the stored values
  * of its W nodes, A_{l^W_T(j), l^W_T(j)} / mult_{l^W_T(j)}, for GLOBAL, and
  * E_INVALID_ARG for QP. */
 int dogip_weights_ex(dogip_mesh mesh, int form, const dogip_coeff* coeff, int quad_n1d, int storage,

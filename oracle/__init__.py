@@ -20,8 +20,12 @@ Modules
   metrics      CSR memory model and efficiencies (eq:memory_eff,
                eq:comp_eff)
 
-Parity pins: every function is pinned by tests/test_oracle_*.py (see
-DESIGN.md "Oracle pins").  None is "parity unpinned" except the Table 1/2
-``mem A`` column for k>=2 (coefficient-dependent drops, reading L13), which
-the oracle does not claim to reproduce.
+Parity pins (DESIGN.md section 3 lists one named pin per function):
+tests/test_oracle_reference.py, test_oracle_tables.py, test_oracle_assemble.py,
+test_oracle_cg.py and test_oracle_sampled_and_coefficients.py (the full-size
+sampled-row checker ``assemble.apply_rows_sampled`` / ``mesh.cell_elements``
+against the CSR route on every (d, p, form), and the coefficient closed forms:
+Rodrigues rotations, the {1, 10, 100} spectrum, tanh / sin-cos point values).
+Parity unpinned: only the Table 1/2 ``mem A`` column for k>=2 (coefficient-
+dependent drops, reading L13), which the oracle does not claim to reproduce.
 """

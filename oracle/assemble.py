@@ -11,8 +11,11 @@ Never uses double-grid weights.
 
 Routes: CSR (scipy.sparse) for small meshes; element route (y = sum_T
 P_T^T K_T P_T u, the "alternative approaches" form of P:66-75) for big meshes;
-``apply_rows`` computes selected entries of A u one by one for full-size
-sampled parity.
+quadrature-point route (interpolate u_T to the rule's points, scale by the
+coefficient and |det R_T| w_q, project back: the same sum without forming K_T,
+P:61-75) for the full-size C3 / C5 residual checks; ``apply_rows`` /
+``apply_rows_sampled`` compute selected entries of A u one by one for
+full-size sampled parity.
 """
 from __future__ import annotations
 
@@ -33,11 +36,21 @@ class ElementData:
     def __init__(self, mesh: Mesh, p: int, n1d: int | None = None):
         self.mesh, self.p, self.d = mesh, p, mesh.d
         self.R, self.S, self.det, self.Rinv = affine_maps(mesh)
-        self.lT = dof_map(mesh, p)
+        self._lT = None
         self.qp, self.qw = simplex_rule(mesh.d, n1d or contract_n1d(p))
         self.Phi = eval_basis(mesh.d, p, self.qp)          # (nq, V_T)
         self.dPhi = eval_grad(mesh.d, p, self.qp)          # (nq, V_T, d)
         self.ndof = (p * mesh.N + 1) ** mesh.d
+
+    @property
+    def lT(self) -> np.ndarray:
+        """l_T of every element (computed on first use; full-size routes use lT_of)."""
+        if self._lT is None:
+            self._lT = dof_map(self.mesh, self.p)
+        return self._lT
+
+    def lT_of(self, sl: slice) -> np.ndarray:
+        return self._lT[sl] if self._lT is not None else dof_map(self.mesh, self.p, sl)
 
     def element_matrices(self, form: int, coef, sl: slice) -> np.ndarray:
         """K_T for elements in ``sl`` -> (nb, V_T, V_T)."""
@@ -203,3 +216,76 @@ def apply_rows_sampled(d: int, N: int, p: int, vertices, form: int, coef, u: np.
                 acc += K[e, hit[0]] @ u[ed.lT[e]]
         out[n] = acc
     return out
+
+
+def _qp_chunk(ed: ElementData, form: int, coef, uu: np.ndarray, sl: slice):
+    """One chunk of the quadrature-point route: (l_T, y_T) of the elements in sl."""
+    d = ed.d
+    R, S, det, Rinv = ed.R[sl], ed.S[sl], ed.det[sl], ed.Rinv[sl]
+    nb, nq = R.shape[0], ed.qp.shape[0]
+    l = ed.lT_of(sl)
+    uT = uu[l]                                                     # P_T u   (nb, V_T)
+    x = np.einsum("eij,qj->eqi", R, ed.qp) + S[:, None, :]         # F_T(xq)
+    c = coefs.evaluate(coef, d, x.reshape(-1, d), np.repeat(ed.mesh.cell[sl], nq))
+    scale = np.abs(det)[:, None] * ed.qw[None, :]                  # |det R_T| w_q
+    if form == FORM_WP:
+        if c.ndim != 1:
+            raise ValueError("WP needs a scalar coefficient")
+        uq = uT @ ed.Phi.T                                         # u_h(xq)        (nb, nq)
+        yT = (scale * c.reshape(nb, nq) * uq) @ ed.Phi             # sum_q w m u phi_i
+        return l, yT
+    Mq = coefs.as_tensor(c, d).reshape(nb, nq, d, d)
+    VT = uT.shape[1]
+    gref = (uT @ ed.dPhi.transpose(1, 0, 2).reshape(VT, nq * d)).reshape(nb, nq, d)  # reference gradient
+    g = np.einsum("epr,eqp->eqr", Rinv, gref)                      # R^-T grad_hat  (eq:bas_deriv)
+    flux = scale[:, :, None] * np.einsum("eqrs,eqs->eqr", Mq, g)   # |det| w_q M grad u
+    t = np.einsum("epr,eqr->eqp", Rinv, flux)                      # R^-1 flux
+    yT = t.reshape(nb, nq * d) @ ed.dPhi.transpose(0, 2, 1).reshape(nq * d, VT)  # sum_q grad_hat phi_l . (R^-1 flux)
+    return l, yT
+
+
+def apply_qp_route(ed: ElementData, form: int, coef, u: np.ndarray, dirichlet: bool = False,
+                   workers: int = 1, chunk: int = 8192) -> np.ndarray:
+    """y = A u by the quadrature-point route: for every element,
+    u_T -> values / physical gradients at the contract rule's points -> times
+    |det R_T| w_q m (WP) or |det R_T| w_q M (EL) -> tested against phi_i /
+    grad phi_i, summed into y.  Algebraically sum_T P_T^T K_T P_T u with the K_T
+    of element_matrices (same rule); no K_T and no global matrix are formed, so it
+    runs at the full C3 / C5 sizes.  ``workers`` > 1 evaluates chunks in threads
+    (NumPy releases the GIL in its kernels); the sum into y stays sequential."""
+    mask = boundary_mask(ed.d, ed.mesh.N, ed.p) if dirichlet else None
+    uu = np.where(mask, 0.0, u) if dirichlet else u
+    y = np.zeros(ed.ndof)
+    sls = list(ed.chunks(chunk))
+    if workers <= 1:
+        parts = (_qp_chunk(ed, form, coef, uu, sl) for sl in sls)
+        for l, yT in parts:
+            y += np.bincount(l.ravel(), weights=yT.ravel(), minlength=ed.ndof)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(workers) as ex:
+            for l, yT in ex.map(lambda sl: _qp_chunk(ed, form, coef, uu, sl), sls):
+                y += np.bincount(l.ravel(), weights=yT.ravel(), minlength=ed.ndof)
+    if dirichlet:
+        y[mask] = u[mask]
+    return y
+
+
+def wp_total(ed: ElementData, coef, workers: int = 1, chunk: int = 16384) -> float:
+    """1^T A 1 of the weighted projection = sum_T |det R_T| sum_q w_q m(F_T xq)
+    (sum_i phi_i = 1, so sum_ij K_T,ij is the rule's integral of m over T; equally
+    sum_T sum_j a_{T,j} of Theorem 2's weights, since sum_j phi^W_j = 1)."""
+    d, nq = ed.d, ed.qp.shape[0]
+
+    def part(sl):
+        R, S, det = ed.R[sl], ed.S[sl], ed.det[sl]
+        x = np.einsum("eij,qj->eqi", R, ed.qp) + S[:, None, :]
+        c = coefs.evaluate(coef, d, x.reshape(-1, d), np.repeat(ed.mesh.cell[sl], nq))
+        return float((np.abs(det)[:, None] * ed.qw[None, :] * c.reshape(-1, nq)).sum())
+
+    sls = list(ed.chunks(chunk))
+    if workers <= 1:
+        return sum(part(sl) for sl in sls)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(workers) as ex:
+        return sum(ex.map(part, sls))

@@ -66,7 +66,7 @@ def evaluate(coef: Coefficient, d: int, x: np.ndarray, cell: np.ndarray) -> np.n
         omega = np.stack([(c[:, i][None, :] * np.cos(arg + phi[:, i][None, :])).sum(axis=1)
                           for i in range(3)], axis=1)
         R = rodrigues(omega)
-        return np.einsum("nij,j,nkj->nik", R, eig, R)
+        return (R * eig[None, None, :]) @ np.transpose(R, (0, 2, 1))    # R diag(eig) R^T
     if k == COEF_CONST_TENSOR:
         Mm = P[:d * d].reshape(d, d)
         return np.broadcast_to(Mm, (x.shape[0], d, d)).copy()

@@ -67,20 +67,6 @@ def algorithm1(ed: ElementData, form: int, weights: np.ndarray, u: np.ndarray) -
     return v
 
 
-def algorithm1_batched(ed: ElementData, form: int, weights: np.ndarray,
-                       u: np.ndarray) -> np.ndarray:
-    """Algorithm 1 with the element loop batched (same arithmetic per element)."""
-    d = ed.d
-    B = bhat_wp(d, ed.p) if form == FORM_WP else bhat_el(d, ed.p)
-    uT = u[ed.lT]
-    if form == FORM_WP:
-        yT = np.einsum("jk,ej->ek", B, weights * np.einsum("jl,el->ej", B, uT))
-    else:
-        g = np.einsum("sjl,el->ejs", B, uT)
-        yT = np.einsum("rjk,ejr->ek", B, np.einsum("ejrs,ejs->ejr", weights, g))
-    return np.bincount(ed.lT.ravel(), weights=yT.ravel(), minlength=ed.ndof)
-
-
 def dense_elementwise_operator(ed: ElementData, form: int, weights: np.ndarray) -> np.ndarray:
     """Check (iv): dense global B (rows = (T, j[, r])) and block-diagonal
     A^DoGIP, returning C^T A^DoGIP B with C = B."""

@@ -80,13 +80,13 @@ def structured_mesh(d: int, N: int, vertices: Optional[np.ndarray] = None) -> Me
     return Mesh(d, N, vlat, X, elems, cell)
 
 
-def dof_map(mesh: Mesh, p: int) -> np.ndarray:
+def dof_map(mesh: Mesh, p: int, sl: slice = slice(None)) -> np.ndarray:
     """l_T: (ne, V_T) global DoF ids of C_{N,p}; local order of
-    reference.multi_indices (L5)."""
+    reference.multi_indices (L5).  ``sl`` restricts to a range of elements."""
     d, N = mesh.d, mesh.N
     Md = p * N + 1
     A = np.array(multi_indices(d, p))                    # (V_T, d+1)
-    cv = mesh.vlat[mesh.elems]                           # (ne, d+1, d)
+    cv = mesh.vlat[mesh.elems[sl]]                       # (ne, d+1, d)
     lat = np.einsum("la,eac->elc", A, cv)                # (ne, V_T, d)
     return sum(lat[:, :, a] * Md ** a for a in range(d)).astype(np.int64)
 

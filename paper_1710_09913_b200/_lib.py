@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdogip.so")
 
 DOGIP_WP, DOGIP_EL = 0, 1
-DOGIP_STORE_FULL, DOGIP_STORE_ISO, DOGIP_STORE_GLOBAL, DOGIP_STORE_PAIR, DOGIP_STORE_QP, DOGIP_STORE_SYM = 0, 1, 2, 3, 4, 5
+DOGIP_STORE_FULL, DOGIP_STORE_ISO, DOGIP_STORE_GLOBAL, DOGIP_STORE_QP, DOGIP_STORE_SYM = 0, 1, 2, 4, 5
 DOGIP_DIRICHLET_ZERO, DOGIP_NO_EXCHANGE, DOGIP_CG_RESUME = 1, 2, 4
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "E_INVALID_DIM", -2: "E_INVALID_SIZE",
           -3: "E_UNSUPPORTED_ORDER", -4: "E_DEGENERATE_ELEMENT", -5: "E_BAD_COEFF", -6: "E_OOM",

@@ -43,6 +43,8 @@ def _tensor_ptr(t, n: int, device: Optional[int] = None) -> int:
         raise ValueError(f"expected {n} entries, got {t.numel()}")
     if device is not None and t.device.index != device:
         raise ValueError(f"tensor on cuda:{t.device.index}, mesh on cuda:{device}")
+    if t.data_ptr() % 16:
+        raise ValueError("vector must be 16-byte aligned (the C ABI reads fp64 pairs)")
     return t.data_ptr()
 
 

@@ -93,6 +93,28 @@ struct dogip_op_s {
     std::vector<cudaEvent_t> ev_in, ev_done;
 };
 
+// Makes `dev` current for the scope and restores the caller's device afterwards (setup,
+// destroy and synchronous entry points must not leave torch's current device switched).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Caller vectors are read and written as 16-byte pairs by the CG / reduction kernels.
+static int check_vec(const void* p, const char* name) {
+    if (!p) return fail(DOGIP_E_INVALID_ARG, std::string("null ") + name);
+    if ((reinterpret_cast<uintptr_t>(p) & 15u) != 0)
+        return fail(DOGIP_E_INVALID_ARG, std::string(name) + " must be 16-byte aligned");
+    return DOGIP_OK;
+}
+
 static int64_t ipow(int64_t b, int e) {
     int64_t r = 1;
     while (e--) r *= b;
@@ -146,9 +168,9 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
     g.fd_ns = make_fastdiv((uint32_t)g.ns);
     g.fd_nxb = make_fastdiv((uint32_t)g.nxb);
     g.fd_ny = make_fastdiv((uint32_t)g.Ny);
-    if (2 * g.ntiles >= (int64_t)1 << 31) {   // tile_coord's 32-bit arithmetic (half-tiles of PAIR)
+    if (g.ntiles >= (int64_t)1 << 31) {   // tile_coord's 32-bit arithmetic
         delete m;
-        return fail(DOGIP_E_INVALID_SIZE, "invalid-size: more than 2^30 element tiles per rank");
+        return fail(DOGIP_E_INVALID_SIZE, "invalid-size: 2^31 or more element tiles per rank");
     }
     g.sy = M;
     g.sz = d == 3 ? M * M : 0;
@@ -185,6 +207,7 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
         *out = m;
         return DOGIP_OK;
     }
+    DeviceGuard dg(device);
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) { delete m; return fail(DOGIP_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e)); }
     cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
@@ -233,7 +256,7 @@ extern "C" int dogip_mesh_info(dogip_mesh m, dogip_mesh_info_t* o) {
 extern "C" void dogip_mesh_destroy(dogip_mesh m) {
     if (!m) return;
     if (m->device < 0) { delete m; return; }
-    cudaSetDevice(m->device);
+    DeviceGuard dg(m->device);
     if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
     if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
     if (m->ev_bnd) cudaEventDestroy(m->ev_bnd);
@@ -341,10 +364,10 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     *out = nullptr;
     if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
     if (storage != DOGIP_STORE_FULL && storage != DOGIP_STORE_ISO && storage != DOGIP_STORE_GLOBAL &&
-        storage != DOGIP_STORE_PAIR && storage != DOGIP_STORE_QP && storage != DOGIP_STORE_SYM)
+        storage != DOGIP_STORE_QP && storage != DOGIP_STORE_SYM)
         return fail(DOGIP_E_INVALID_ARG, "unknown storage");
-    if ((storage == DOGIP_STORE_PAIR || storage == DOGIP_STORE_SYM) && form != DOGIP_WP)
-        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_PAIR / DOGIP_STORE_SYM apply to the weighted projection only");
+    if (storage == DOGIP_STORE_SYM && form != DOGIP_WP)
+        return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_SYM applies to the weighted projection only");
     if (storage == DOGIP_STORE_ISO && form != DOGIP_EL)
         return fail(DOGIP_E_INVALID_ARG, "DOGIP_STORE_ISO applies to the elliptic form only");
     if (storage == DOGIP_STORE_GLOBAL && form != DOGIP_WP)
@@ -356,7 +379,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     RET(check_coeff(m->d, form, coeff, ncomp));
     if (storage == DOGIP_STORE_ISO && ncomp != 1)
         return fail(DOGIP_E_BAD_COEFF, "DOGIP_STORE_ISO needs an isotropic coefficient (M = m I)");
-    CK(cudaSetDevice(m->device));
+    DeviceGuard dg(m->device);
     cudaStream_t st = (cudaStream_t)stream;
     const int d = m->d, p = m->p;
     auto* op = new dogip_op_s();
@@ -421,8 +444,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     DevBufs tmp;
     WeightsArgs a{};
     a.d = d; a.p = p; a.form = form;
-    a.store = (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_PAIR || storage == DOGIP_STORE_SYM) ? 0 : storage;
-    a.pair = storage == DOGIP_STORE_PAIR;
+    a.store = (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_SYM) ? 0 : storage;
     a.sym = storage == DOGIP_STORE_SYM;
     a.nq = nq; a.WT = WT; a.NC = NC; a.ncomp = ncomp;
     a.NG = op->ref.NG; a.tile_rows = op->ref.tile_rows;
@@ -462,7 +484,7 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         a.symj = dj;
         a.symc = dc;
     }
-    if (a.pair || op->ref.has_rowperm) {
+    if (op->ref.has_rowperm) {
         int* drp = nullptr;
         if (tmp.alloc(&drp, WT)) return cleanup_fail(DOGIP_E_OOM, "row permutation");
         cudaMemcpy(drp, op->ref.rowperm, sizeof(int) * WT, cudaMemcpyHostToDevice);
@@ -557,7 +579,7 @@ extern "C" int dogip_op_info(dogip_op op, dogip_op_info_t* o) {
 
 extern "C" void dogip_op_destroy(dogip_op op) {
     if (!op) return;
-    cudaSetDevice(op->m->device);
+    DeviceGuard dg(op->m->device);
     for (double* x : {op->d_w, op->d_sV, op->r, op->pv, op->q, op->partials, op->scal, op->hu, op->hy, op->dotp,
                       op->bpart})
         cudaFree(x);
@@ -616,13 +638,6 @@ static QpArgs qp_args(dogip_op op, const ApplyArgs& a) {
     q.num_sms = a.num_sms; q.stream = a.stream;
     q.dot_partials = a.dot_partials; q.dot_nslots = a.dot_nslots;
     return q;
-}
-
-// The paired-lane WP kernel (DOGIP_STORE_PAIR) has no boundary masks.
-static int check_dirichlet_storage(dogip_op op, unsigned flags) {
-    if ((flags & DOGIP_DIRICHLET_ZERO) && op->store == DOGIP_STORE_PAIR)
-        return fail(DOGIP_E_INVALID_ARG, "DOGIP_DIRICHLET_ZERO is not supported with DOGIP_STORE_PAIR");
-    return DOGIP_OK;
 }
 
 // y = A u (+ exchange); with dot != null also *dot = u^T y over this rank's elements
@@ -692,10 +707,11 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
 }
 
 extern "C" int dogip_apply(dogip_op op, const double* u, double* y, unsigned flags, void* stream) {
-    if (!op || !u || !y) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (!op) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    RET(check_vec(u, "u"));
+    RET(check_vec(y, "y"));
     if (u == y) return fail(DOGIP_E_INVALID_ARG, "u and y must not alias");
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
-    RET(check_dirichlet_storage(op, flags));
     return apply_impl(op, u, y, flags, (cudaStream_t)stream);
 }
 
@@ -768,10 +784,9 @@ static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_hos
 extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_host, unsigned flags, void* stream) {
     if (!op || !u_host || !y_host) return fail(DOGIP_E_INVALID_ARG, "null argument");
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
-    RET(check_dirichlet_storage(op, flags));
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = op->m->geo.ndof;
-    CK(cudaSetDevice(op->m->device));
+    DeviceGuard dg(op->m->device);
     if (!op->hu) {
         CK(cudaMalloc(&op->hu, sizeof(double) * n));
         CK(cudaMalloc(&op->hy, sizeof(double) * n));
@@ -786,7 +801,8 @@ extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_hos
 }
 
 extern "C" int dogip_load_vector(dogip_op op, double f, double* b, unsigned flags, void* stream) {
-    if (!op || !b) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (!op) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    RET(check_vec(b, "b"));
     cudaStream_t st = (cudaStream_t)stream;
     dogip_mesh_s* m = op->m;
     CK(cudaMemsetAsync(b, 0, sizeof(double) * m->geo.ndof, st));
@@ -870,9 +886,10 @@ static int cg_graph_run(dogip_op op, cudaStream_t st, int* iters) {
 
 extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, int maxit, unsigned flags,
                         void* stream, dogip_cg_result* res) {
-    if (!op || !b || !x || !res) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (!op || !res) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    RET(check_vec(b, "b"));
+    RET(check_vec(x, "x"));
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_CG_RESUME)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
-    RET(check_dirichlet_storage(op, flags));
     cudaStream_t st = (cudaStream_t)stream;
     dogip_mesh_s* m = op->m;
     const int64_t n = m->geo.ndof;
@@ -1112,7 +1129,7 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
     const int NC = op->form == DOGIP_WP ? 1 : d * (d + 1) / 2;
     if (cap < info.n_elem_local * WT * NC) return fail(DOGIP_E_INVALID_SIZE, "capacity too small");
     std::vector<double> w(op->w_doubles);
-    CK(cudaSetDevice(op->m->device));
+    DeviceGuard dg(op->m->device);
     CK(cudaMemcpy(w.data(), op->d_w, sizeof(double) * op->w_doubles, cudaMemcpyDeviceToHost));
     const SlabGeo& g = op->m->geo;
     std::vector<int> offw;
@@ -1130,11 +1147,7 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
                 for (int j = 0; j < WT; ++j) host[e * WT + j] = w[bw + offw[(size_t)tc.s * WT + j]];
                 continue;
             }
-            auto at = [&](int row) {
-                if (op->store == DOGIP_STORE_PAIR)   // half-tiles of 16, node rows permuted
-                    return w[((size_t)(2 * t + lane / 16) * TR + op->ref.rowperm[row]) * 16 + lane % 16];
-                return w[((size_t)t * TR + row) * TILE + lane];
-            };
+            auto at = [&](int row) { return w[((size_t)t * TR + row) * TILE + lane]; };
             if (op->store == DOGIP_STORE_SYM) {
                 // a_j = sum over the rows r of j's orbit of s_r c_{r,j} ahat_r  (the character
                 // matrix of an orbit is orthogonal: X X^T = s I)

@@ -270,158 +270,6 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
     std::fprintf(f, "};\n\n");
 }
 
-// Paired-lane WP variant (STORE 3): two lanes share one element.  sigma is an
-// involution of the barycentric indices (3D (0 1)(2 3), 2D (0 1)); Bhat is
-// sigma-invariant, Bhat[sigma beta, sigma alpha] = Bhat[beta, alpha], because the
-// product basis is.  Lane 0 holds the DoFs of a fundamental domain A
-// of sigma plus its fixed DoFs F ("view slots"); lane 1 holds sigma(A) and F in
-// the same slots, so both lanes run the same code with the same constants:
-//   Q_j = sum_{m in A} Bhat[j,m] U_m + 1/2 sum_{f in F} Bhat[j,f] U_f   (view node j)
-//   g_j = Q_j + partner's Q_{sigma j}       (one shuffle; = (Bhat u_T)_j of the lane's view)
-//   h_j = a_j g_j,   Y_m += Bhat[j,m] h_j  (m in A u F; lane 1 does not scatter F)
-// Node pairs (j, sigma j) are stored in adjacent weight rows (2i, 2i+1), fixed
-// nodes after them; lane k reads row 2i+k for view node j_i and 2i+1-k for
-// sigma j_i, so the per-lane weight permutation costs no instructions.
-static void emit_pair(FILE* f, int d, int p) {
-    Table t = bhat_table(d, p, 0);
-    const int VT = t.cols, WT = t.rows;
-    auto A = multi_indices(d, p);
-    auto W = multi_indices(d, 2 * p);
-    const int sig[4] = {1, 0, d == 3 ? 3 : 2, d == 3 ? 2 : 3};
-    auto perm = [&](const std::array<int, 4>& a) {
-        std::array<int, 4> b{};
-        for (int i = 0; i <= d; ++i) b[i] = a[sig[i]];
-        return b;
-    };
-    auto find = [](const std::vector<std::array<int, 4>>& v, const std::array<int, 4>& a) {
-        for (size_t i = 0; i < v.size(); ++i)
-            if (v[i] == a) return (int)i;
-        std::fprintf(stderr, "pair: index not found\n");
-        std::exit(1);
-    };
-    std::vector<int> sA(VT), sW(WT);
-    for (int l = 0; l < VT; ++l) sA[l] = find(A, perm(A[l]));
-    for (int j = 0; j < WT; ++j) sW[j] = find(W, perm(W[j]));
-    for (int j = 0; j < WT; ++j)
-        for (int l = 0; l < VT; ++l)
-            if (t.at(0, j, l) != t.at(0, sW[j], sA[l])) { std::fprintf(stderr, "pair: Bhat not sigma-invariant\n"); std::exit(1); }
-    std::vector<int> slot, fixed;   // lane-0 local DoF of each view slot: A slots, then F slots
-    std::vector<bool> used(VT, false);
-    for (int l = 0; l < VT; ++l) {
-        if (sA[l] == l) { fixed.push_back(l); continue; }
-        if (used[l]) continue;
-        slot.push_back(l);
-        used[l] = used[sA[l]] = true;
-    }
-    const int NFIX = (int)fixed.size();
-    slot.insert(slot.end(), fixed.begin(), fixed.end());
-    const int VS = (int)slot.size();
-    std::vector<int> rowperm(WT, -1), rownode;   // rownode[r] = canonical node in storage row r
-    for (int j = 0; j < WT; ++j)
-        if (sW[j] > j) { rownode.push_back(j); rownode.push_back(sW[j]); }
-    const int NPAIR = (int)rownode.size() / 2;
-    for (int j = 0; j < WT; ++j)
-        if (sW[j] == j) rownode.push_back(j);
-    for (int r = 0; r < WT; ++r) rowperm[rownode[r]] = r;
-    int nnz = 0, pm1 = 0;
-    for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
-    auto simp = cell_simplices(d);
-    std::fprintf(f, "template <> struct RefElem<%d, %d, 0, 3> {\n", d, p);
-    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = 2, PAIR = 1, DOT_IN_BODY = 0, HAS_ROWPERM = 1;\n",
-                 VT, WT, WT, (int)simp.size());
-    std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d;\n", nnz, pm1);
-    std::fprintf(f, "    static constexpr int VS = %d, NFIX = %d, NPAIR = %d;\n", VS, NFIX, NPAIR);
-    std::fprintf(f, "    static constexpr signed char SIGMA[4] = {%d, %d, %d, %d};\n", sig[0], sig[1], sig[2], sig[3]);
-    std::fprintf(f, "    static __host__ __device__ constexpr int sigma(int i) { return i == 0 ? %d : i == 1 ? %d : i == 2 ? %d : %d; }\n",
-                 sig[0], sig[1], sig[2], sig[3]);
-    std::fprintf(f, "    static constexpr signed char SLOT_ALPHA[%d][3] = {", VS);
-    for (int m = 0; m < VS; ++m)
-        std::fprintf(f, "%s{%d,%d,%d}", m ? "," : "", A[slot[m]][1], A[slot[m]][2], d == 3 ? A[slot[m]][3] : 0);
-    std::fprintf(f, "};\n");
-    std::fprintf(f, "    static constexpr short SLOT_DOF[%d] = {", VS);
-    for (int m = 0; m < VS; ++m) std::fprintf(f, "%s%d", m ? "," : "", slot[m]);
-    std::fprintf(f, "};\n");
-    std::fprintf(f, "    static constexpr short ROWPERM[%d] = {", WT);
-    for (int j = 0; j < WT; ++j) std::fprintf(f, "%s%d", j ? "," : "", rowperm[j]);
-    std::fprintf(f, "};\n");
-    std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
-    for (size_t s = 0; s < simp.size(); ++s) {
-        std::fprintf(f, "%s{", s ? ", " : "");
-        for (int l = 0; l < VT; ++l) {
-            std::fprintf(f, "%s{", l ? "," : "");
-            for (int ax = 0; ax < d; ++ax) {
-                int o = 0;
-                for (int i = 0; i <= d; ++i) o += A[l][i] * simp[s][i][ax];
-                std::fprintf(f, "%s%d", ax ? "," : "", o);
-            }
-            std::fprintf(f, "}");
-        }
-        std::fprintf(f, "}");
-    }
-    std::fprintf(f, "};\n");
-    std::fprintf(f, "    static __host__ __device__ constexpr int row_of(int r) { return r; }\n");
-    std::fprintf(f,
-        "    template <class Pol>\n"
-        "    static __device__ __forceinline__ void body(const double* __restrict__ u,\n"
-        "                                                double* __restrict__ y, Pol& pol) {\n");
-    int flops = 0;   // per lane
-    auto interp_terms = [&](int j) {
-        std::vector<std::pair<int, Rat>> terms;
-        for (int m = 0; m < VS; ++m) {
-            Rat c = t.at(0, j, slot[m]);
-            if (c.is_zero()) continue;
-            if (m >= VS - NFIX) c = c * Rat(1, 2);
-            terms.push_back({m, c});
-        }
-        return terms;
-    };
-    auto project = [&](int j, const std::string& h) {
-        for (int m = 0; m < VS; ++m) {
-            const Rat c = t.at(0, j, slot[m]);
-            if (c.is_zero()) continue;
-            std::string acc = "y[" + std::to_string(m) + "]";
-            if (c == Rat(1)) acc = "(" + acc + ") + " + h;
-            else if (c == Rat(-1)) acc = "(" + acc + ") - " + h;
-            else { acc = "__fma_rn(" + lit(c.to_double()) + ", " + h + ", " + acc + ")"; flops += 1; }
-            flops += 1;
-            std::fprintf(f, "          y[%d] = %s;\n", m, acc.c_str());
-        }
-    };
-    for (int i = 0; i < NPAIR; ++i) {
-        const int ja = rownode[2 * i], jb = rownode[2 * i + 1];
-        auto ta = interp_terms(ja), tb = interp_terms(jb);
-        std::fprintf(f, "        {\n          pol.template begin<%d>();\n", 2 * i);
-        flops += emit_combo(f, "          ", "qa", true, ta, "u");
-        flops += emit_combo(f, "          ", "qb", true, tb, "u");
-        // g_a = qa + partner's qb (its view of sigma j_a = j_b), g_b = qb + partner's qa
-        const bool za = ta.empty(), zb = tb.empty();
-        std::fprintf(f, "          const double ga = %s;\n",
-                     zb ? "qa" : (za ? "pol.xchg(qb)" : "qa + pol.xchg(qb)"));
-        std::fprintf(f, "          const double gb = %s;\n",
-                     za ? "qb" : (zb ? "pol.xchg(qa)" : "qb + pol.xchg(qa)"));
-        flops += (!za && !zb) ? 2 : 0;
-        std::fprintf(f, "          const double ha = pol.wself(%d) * ga;\n", 2 * i);
-        std::fprintf(f, "          const double hb = pol.wother(%d) * gb;\n", 2 * i);
-        flops += 2;
-        project(ja, "ha");
-        project(jb, "hb");
-        std::fprintf(f, "        }\n");
-    }
-    for (int r = 2 * NPAIR; r < WT; ++r) {
-        const int jf = rownode[r];
-        auto tf = interp_terms(jf);
-        std::fprintf(f, "        {\n          pol.template begin<%d>();\n", r);
-        flops += emit_combo(f, "          ", "qf", true, tf, "u");
-        std::fprintf(f, "          const double hf = pol.wfix(%d) * (qf + pol.xchg(qf));\n", r);
-        flops += 2;
-        project(jf, "hf");
-        std::fprintf(f, "        }\n");
-    }
-    std::fprintf(f, "    }\n");
-    std::fprintf(f, "    static constexpr int FLOPS = %d;   // per element (both lanes)\n", 2 * flops);
-    std::fprintf(f, "};\n\n");
-}
-
 // Symmetry-adapted WP variant (STORE 5).  G = an abelian group of commuting
 // barycentric involutions (3D: <(0 1), (2 3)>, 2D: <(0 1)>).  Bhat is G-equivariant,
 // Bhat[g beta, g alpha] = Bhat[beta, alpha] (product basis), so in
@@ -981,7 +829,6 @@ int main(int argc, char** argv) {
             emit_variant(f, d, p, 1, 0);
             if (g_iso_sym) emit_iso_sym(f, d, p);
             else emit_variant(f, d, p, 1, 1);
-            emit_pair(f, d, p);
             emit_sym(f, d, p);
         }
     std::fprintf(f, "}  // namespace dogip_gen\n");

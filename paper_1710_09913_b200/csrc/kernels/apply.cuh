@@ -13,6 +13,33 @@ namespace dogip {
 extern std::atomic<long long> g_launches;
 inline void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Dynamic-shared-memory opt-in and occupancy of one kernel, cached PER DEVICE (the
+// attribute is a per-device property: a second mesh on another device must opt in
+// again).  `cache` is a per-kernel static array; slot = (smem + 1) << 16 | occupancy.
+// Concurrent first calls may both configure, which is harmless.
+constexpr int MAX_DEVICES = 64;
+template <class Kern>
+inline cudaError_t kernel_occupancy(Kern kern, int threads, size_t smem, std::atomic<uint64_t>* cache, int* occ) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t key = ((uint64_t)smem + 1) << 16;
+    std::atomic<uint64_t>* slot = (dev >= 0 && dev < MAX_DEVICES) ? &cache[dev] : nullptr;
+    if (slot) {
+        const uint64_t v = slot->load(std::memory_order_acquire);
+        if ((v & ~0xffffull) == key) { *occ = (int)(v & 0xffff); return cudaSuccess; }
+    }
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (o < 1) o = 1;
+    if (slot) slot->store(key | (uint64_t)(o & 0xffff), std::memory_order_release);
+    *occ = o;
+    return cudaSuccess;
+}
+
 #ifndef DOGIP_APPLY_THREADS
 #define DOGIP_APPLY_THREADS 128
 #endif
@@ -36,7 +63,7 @@ constexpr int MAX_WT_GLOBAL = 165;   // W_T of P_8 in 3D (global WP storage, p <
 
 struct ApplyArgs {
     int d, p, form, store;      // store: 0 full A_T blocks, 1 isotropic a_j + G_T (EL), 2 global WP,
-                                // 3 full WP in the paired-lane layout, 5 symmetry-adapted WP
+                                // 5 symmetry-adapted WP
     bool dirichlet;
     const double* u;
     double* y;
@@ -56,9 +83,8 @@ cudaError_t launch_apply(const ApplyArgs& a);
 // Constants of the generated reference element (generated/bhat_gen.cuh).
 struct RefInfo {
     int VT, WT, NC, NG, NS, tile_rows, flops, nnz, nnz_pm1;
-    int pair;                        // paired-lane WP layout (STORE 3): half-tiles of 16, rows permuted
     int loff[MAX_NS][MAX_VT][3];
-    int has_rowperm;                 // node rows stored permuted (PAIR, symmetry-adapted ISO)
+    int has_rowperm;                 // node rows stored permuted (symmetry-adapted ISO)
     int rowperm[MAX_WT_GLOBAL];      // storage row of canonical node j (identity unless has_rowperm)
     int sym;                         // symmetry-adapted WP (STORE 5): row r = sum_k symc[r][k] a_{symj[r][k]}
     int symj[MAX_WT_GLOBAL][4];
@@ -85,8 +111,7 @@ struct WeightsArgs {
     double* scratch_a;                     // [nb * ncomp][WT]
     int64_t batch;                         // elements per batch (multiple of 32)
     int* bad_flag;                         // device int: 1 degenerate element, 2 bad coefficient
-    int pair;                              // paired-lane WP layout (STORE 3)
-    const int* rowperm;                    // device (WT,): storage row of node j (pair layout)
+    const int* rowperm;                    // device (WT,): storage row of node j (permuted ISO layout)
     int sym;                               // symmetry-adapted WP rows (STORE 5)
     const int* symj;                       // device (WT, 4): canonical nodes of stored row r (-1: none)
     const double* symc;                    // device (WT, 4): their coefficients

@@ -10,7 +10,6 @@ bool ref_info_3_1(int form, int store, RefInfo& r) {
     if (form == 0 && store == 0) { fill_info<3, 1, 0, 0>(r); return true; }
     if (form == 1 && store == 0) { fill_info<3, 1, 1, 0>(r); return true; }
     if (form == 1 && store == 1) { fill_info<3, 1, 1, 1>(r); return true; }
-    if (form == 0 && store == 3) { fill_info<3, 1, 0, 3>(r); return true; }
     if (form == 0 && store == 5) { fill_info<3, 1, 0, 5>(r); return true; }
     return false;
 }

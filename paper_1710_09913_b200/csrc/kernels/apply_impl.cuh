@@ -74,16 +74,12 @@ namespace {
 #ifndef DOGIP_ROWS_4CTA
 #define DOGIP_ROWS_4CTA 12
 #endif
-#ifndef DOGIP_PAIR_MINB
-#define DOGIP_PAIR_MINB 4    // CTAs/SM of the paired-lane WP kernel (u_T, y_T halves: <= 128 registers)
-#endif
 template <class RE>
 constexpr int min_blocks() {
 #ifdef DOGIP_MINB_OVERRIDE
     return DOGIP_MINB_OVERRIDE;
 #endif
-    if constexpr (RE::PAIR) return DOGIP_PAIR_MINB;   // paired-lane WP (STORE 3)
-    else return RE::VT <= 10 ? DOGIP_MINB_SMALL : RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE;
+    return RE::VT <= 10 ? DOGIP_MINB_SMALL : RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE;
 }
 
 // Balanced chunks of whole nodes: NCH = ceil(TILE_ROWS / ROWS_MAX) chunks of ROWS rows
@@ -104,7 +100,7 @@ constexpr int min_blocks() {
 template <class RE>
 __host__ __device__ constexpr bool lockstep() {
     if constexpr (DOGIP_LOCKSTEP >= 0) return DOGIP_LOCKSTEP != 0;
-    else return !RE::DOT_IN_BODY && !RE::PAIR && (RE::NG > 0 || RE::TILE_ROWS >= 165);
+    else return !RE::DOT_IN_BODY && (RE::NG > 0 || RE::TILE_ROWS >= 165);
 }
 
 template <class RE, int TW = TILE>
@@ -199,7 +195,7 @@ struct WarpStream {
 #define DOGIP_DIRECT_ROWS 6    // tiles with at most this many weight rows skip the smem ring
 #endif
 template <class RE>
-__host__ __device__ constexpr bool direct_weights() { return !RE::DOT_IN_BODY && !RE::PAIR && RE::TILE_ROWS <= DOGIP_DIRECT_ROWS; }
+__host__ __device__ constexpr bool direct_weights() { return !RE::DOT_IN_BODY && RE::TILE_ROWS <= DOGIP_DIRECT_ROWS; }
 
 // weights already in registers (direct-weights path): node rows are compile-time indices
 struct RegPol {
@@ -335,7 +331,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     __shared__ int offw_s[GLOB ? MAX_NS * MAX_WT_GLOBAL : 1];
     constexpr bool DW = direct_weights<RE>() && !GLOB;
     if constexpr (GLOB) {
-        for (int i = threadIdx.x; i < MAX_NS * RE::WT; i += blockDim.x)
+        for (int i = threadIdx.x; i < RE::NS * RE::WT; i += blockDim.x)   // the table holds NS * WT
             offw_s[(i / RE::WT) * MAX_WT_GLOBAL + i % RE::WT] = offw_g[i];
         __syncthreads();
     } else if (DW) {
@@ -450,223 +446,6 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     }
 }
 
-// ------------------------------------------------------------------ paired lanes
-// WP with two lanes per element (generated RefElem<D,P,0,3>, see gen_bhat.cpp
-// emit_pair): lane 2e+k holds the view slots of element e of a 16-element
-// half-tile; weights are stored per half-tile [ht][row][16] with node pairs in
-// adjacent rows.  Halves the registers of u_T and y_T (3D P4: 19 + 19 doubles
-// instead of 35 + 35), doubling the resident warps of the FP64-heavy C5 body.
-constexpr int PTW = 16;     // elements per half-tile
-
-template <class RE>
-struct PairStream {
-    using C = Chunking<RE, PTW>;
-    double* ring;
-    uint32_t bar0;
-    int lane, col, k;      // col = element column e, k = lane parity
-    const double* tptr;
-    int64_t tstride, tiles_left;
-    uint32_t cons;
-    const double* cself;   // row 2i + k of the current stage (column col)
-    const double* cother;  // row 2i + 1 - k
-    const double* cfix;    // row r
-    uint64_t policy;
-
-    template <int K, int CI>
-    __device__ __forceinline__ void issue(uint32_t stage) const {
-        if (K >= tiles_left) return;
-        constexpr int rows = (CI == C::NCH - 1) ? C::LAST : C::ROWS;
-        constexpr uint32_t bytes = (uint32_t)rows * PTW * 8u;
-        const uint32_t bar = bar0 + 8u * stage;
-        mbar_expect_tx(bar, bytes);
-        bulk_g2s_evict_first(smem_u32(ring + (size_t)stage * C::ROWS * PTW),
-                             tptr + K * tstride + (int64_t)CI * C::ROWS * PTW, bytes, bar, policy);
-    }
-    template <int G>
-    __device__ __forceinline__ void prologue_one() {
-        if constexpr (G < C::S - 1) {
-            issue<G / C::NCH, G % C::NCH>((uint32_t)G);
-            prologue_one<G + 1>();
-        }
-    }
-    __device__ __forceinline__ void prologue() { prologue_one<0>(); }
-    template <int R>
-    __device__ __forceinline__ void begin() {
-        constexpr int c_cur = R / C::ROWS;
-        if constexpr (R == 0 || c_cur != (R - 1) / C::ROWS) {
-            constexpr int gi = c_cur + C::S - 1;
-            __syncwarp();
-            if (lane == 0) {
-                fence_proxy_async_smem();
-                issue<gi / C::NCH, gi % C::NCH>((cons + C::S - 1) % C::S);
-            }
-            const uint32_t st = cons % C::S;
-            mbar_wait(bar0 + 8u * st, (cons / C::S) & 1u);
-            cfix = ring + (size_t)st * C::ROWS * PTW + col;
-            cself = cfix + k * PTW;
-            cother = cfix + (1 - k) * PTW;
-            ++cons;
-        }
-    }
-    __device__ __forceinline__ double wself(int r) const { return cself[(r % C::ROWS) * PTW]; }
-    __device__ __forceinline__ double wother(int r) const { return cother[(r % C::ROWS) * PTW]; }
-    __device__ __forceinline__ double wfix(int r) const { return cfix[(r % C::ROWS) * PTW]; }
-    __device__ __forceinline__ double xchg(double v) const { return __shfl_xor_sync(0xffffffffu, v, 1); }
-    __device__ __forceinline__ void next_tile() {
-        tptr += tstride;
-        --tiles_left;
-    }
-};
-
-struct PairCtx {
-    int64_t base;          // DoF index of this lane's view origin (cell origin + p V_0)
-    int w1, w2, w3;        // DoF offsets per unit of alpha_1..alpha_d in this lane's view
-    bool valid;
-};
-
-template <class RE, int D>
-__device__ __forceinline__ PairCtx pair_ctx(const SlabGeo& geo, const ApplyTables& tab, int64_t ht, int col, int k) {
-    const TileCoord tc = tile_coord(geo, ht >> 1);
-    const int ci = tc.ci0 + PTW * (int)(ht & 1) + col;
-    PairCtx c;
-    c.valid = ci < geo.Nx;
-    // lane 1 sees DoF sigma(alpha): off = sum_j alpha_j V_{sigma j}, V_0 = 0 (cell origin),
-    // alpha_0 = p - sum_{j>=1} alpha_j  ->  base + p V'_0 + sum_{j>=1} alpha_j (V'_j - V'_0)
-    const int V[4] = {0, tab.vstr[tc.s][0], tab.vstr[tc.s][1], D == 3 ? tab.vstr[tc.s][2] : 0};
-    int Vk[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) Vk[j] = k ? V[RE::sigma(j)] : V[j];
-    c.base = (int64_t)geo.p * (ci + geo.sy * tc.cj + geo.sz * tc.ck) + (int64_t)geo.p * Vk[0];
-    c.w1 = Vk[1] - Vk[0];
-    c.w2 = Vk[2] - Vk[0];
-    c.w3 = D == 3 ? Vk[3] - Vk[0] : 0;
-    return c;
-}
-
-template <class RE, int M>
-__device__ __forceinline__ int pair_off(const PairCtx& c) {
-    return RE::SLOT_ALPHA[M][0] * c.w1 + RE::SLOT_ALPHA[M][1] * c.w2 + RE::SLOT_ALPHA[M][2] * c.w3;
-}
-
-template <class RE, int M = 0>
-__device__ __forceinline__ void pair_gather(const double* __restrict__ ub, const PairCtx& c, double* U) {
-    if constexpr (M < RE::VS) {
-        U[M] = ldg_f64(ub + pair_off<RE, M>(c));
-        pair_gather<RE, M + 1>(ub, c, U);
-    }
-}
-
-// lane 1 does not scatter the fixed slots (both lanes hold their complete sums)
-template <class RE, int M = 0>
-__device__ __forceinline__ void pair_scatter(double* __restrict__ yb, const PairCtx& c, const double* Y, int k) {
-    if constexpr (M < RE::VS) {
-        if (M < RE::VS - RE::NFIX || k == 0) red_add_f64(yb + pair_off<RE, M>(c), Y[M]);
-        pair_scatter<RE, M + 1>(yb, c, Y, k);
-    }
-}
-
-template <int D, int P>
-__global__ void __launch_bounds__(APPLY_THREADS, min_blocks<dogip_gen::RefElem<D, P, 0, 3>>())
-apply_pair_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
-                  const SlabGeo geo, const ApplyTables tab, const int64_t ht_begin, const int64_t ht_end,
-                  double* __restrict__ dot_partials) {
-    using RE = dogip_gen::RefElem<D, P, 0, 3>;
-    using C = Chunking<RE, PTW>;
-    constexpr int NW = APPLY_THREADS / 32;
-    constexpr int VS = RE::VS, NA = RE::VS - RE::NFIX;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* rings = reinterpret_cast<double*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)NW * C::S * C::ROWS * PTW);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int col = lane >> 1, k = lane & 1;
-    const int64_t gw = ht_begin + (int64_t)blockIdx.x * NW + warp;
-    const int64_t nw = (int64_t)gridDim.x * NW;
-    PairStream<RE> ws;
-    ws.ring = rings + (size_t)warp * C::S * C::ROWS * PTW;
-    ws.bar0 = smem_u32(bars + warp * C::S);
-    ws.lane = lane; ws.col = col; ws.k = k;
-    ws.tptr = w + gw * C::TILE_DBL;
-    ws.tstride = nw * C::TILE_DBL;
-    ws.tiles_left = gw < ht_end ? (ht_end - gw + nw - 1) / nw : 0;
-    ws.cons = 0;
-    ws.policy = policy_evict_first();
-    if (lane == 0) {
-        for (int s = 0; s < C::S; ++s) mbar_init(ws.bar0 + 8u * s, 1);
-        fence_mbar_init();
-        ws.prologue();
-    }
-    __syncwarp();
-
-    double udot = 0.0;
-    double U[VS];
-    PairCtx cur{};
-    auto gather = [&](const PairCtx& c) {
-#pragma unroll
-        for (int m = 0; m < VS; ++m) U[m] = 0.0;
-        if (c.valid) pair_gather<RE>(u + c.base, c, U);
-    };
-    if (gw < ht_end) {
-        cur = pair_ctx<RE, D>(geo, tab, gw, col, k);
-        gather(cur);
-    }
-    for (int64_t ht = gw; ht < ht_end; ht += nw) {
-        double Y[VS];
-#pragma unroll
-        for (int m = 0; m < VS; ++m) Y[m] = 0.0;
-        RE::body(U, Y, ws);
-        ws.next_tile();
-        if (dot_partials) {   // u_T^T y_T: A slots once per lane, fixed slots half in each lane
-#pragma unroll
-            for (int m = 0; m < VS; ++m) udot = fma(m < NA ? U[m] : 0.5 * U[m], Y[m], udot);
-        }
-        const PairCtx prev = cur;
-        if (ht + nw < ht_end) {
-            cur = pair_ctx<RE, D>(geo, tab, ht + nw, col, k);
-            gather(cur);
-        }
-        if (prev.valid) pair_scatter<RE>(y + prev.base, prev, Y, k);
-    }
-    if (dot_partials) {
-        for (int o = 16; o > 0; o >>= 1) udot += __shfl_xor_sync(0xffffffffu, udot, o);
-        if (lane == 0) dot_partials[(int64_t)blockIdx.x * NW + warp] = udot;
-    }
-}
-
-template <int D, int P>
-cudaError_t launch_pair(const ApplyArgs& a) {
-    using RE = dogip_gen::RefElem<D, P, 0, 3>;
-    using C = Chunking<RE, PTW>;
-    constexpr int NW = APPLY_THREADS / 32;
-    const size_t smem = (size_t)NW * C::S * C::ROWS * PTW * 8 + (size_t)NW * C::S * 8;
-    auto kern = apply_pair_kernel<D, P>;
-    static int configured = 0;
-    static int occ = 1;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, APPLY_THREADS, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-        configured = 1;
-    }
-    const int64_t h0 = 2 * a.tile_begin, h1 = 2 * a.tile_end;     // half-tiles
-    const int64_t nht = h1 - h0;
-    int64_t grid = (int64_t)a.num_sms * occ;
-    const int64_t need = (nht + NW - 1) / NW;
-    if (grid > need) grid = need;
-    if (a.dot_partials) {
-        if (grid < 1) grid = 1;
-        if (grid * NW > APPLY_MAX_WARPS) grid = APPLY_MAX_WARPS / NW;
-        *a.dot_nslots = (int)(grid * NW);
-    } else if (nht <= 0) {
-        return cudaSuccess;
-    }
-    kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, h0, h1, a.dot_partials);
-    count_launches(1);
-    return cudaGetLastError();
-}
-
 template <int D, int P, int F, int ST, bool DIR, bool GLOB>
 cudaError_t launch_one(const ApplyArgs& a) {
     using RE = dogip_gen::RefElem<D, P, F, ST>;
@@ -677,16 +456,9 @@ cudaError_t launch_one(const ApplyArgs& a) {
     const size_t smem = (GLOB || DW) ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8 +
                                    (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0);
     auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
-    static int configured = 0;   // per instantiation
-    static int occ = 1;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, APPLY_THREADS, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-        configured = 1;
-    }
+    static std::atomic<uint64_t> cfg[MAX_DEVICES];   // per instantiation, per device
+    int occ = 1;
+    if (cudaError_t e = kernel_occupancy(kern, APPLY_THREADS, smem, cfg, &occ); e != cudaSuccess) return e;
     const int64_t ntiles = a.tile_end - a.tile_begin;
     int64_t grid = (int64_t)a.num_sms * occ;
     const int64_t need = (ntiles + NW - 1) / NW;
@@ -711,11 +483,9 @@ cudaError_t launch_dir(const ApplyArgs& a) {
 
 template <int D, int P>
 cudaError_t launch_form(const ApplyArgs& a) {
-    // Dirichlet elimination (DOGIP_DIRICHLET_ZERO) for every storage but PAIR, whose
-    // paired-lane kernel has no boundary masks (abi.cu rejects that combination)
+    // every storage has the Dirichlet-elimination instantiation (DOGIP_DIRICHLET_ZERO)
     if (a.form == 0 && a.store == 2)
         return a.dirichlet ? launch_one<D, P, 0, 0, true, true>(a) : launch_one<D, P, 0, 0, false, true>(a);
-    if (a.form == 0 && a.store == 3) return launch_pair<D, P>(a);
     if (a.form == 0 && a.store == 5) return launch_dir<D, P, 0, 5>(a);
     if (a.form == 0) return launch_dir<D, P, 0, 0>(a);
     return a.store == 1 ? launch_dir<D, P, 1, 1>(a) : launch_dir<D, P, 1, 0>(a);
@@ -728,7 +498,6 @@ void fill_info(RefInfo& r) {
     r.VT = RE::VT; r.WT = RE::WT; r.NC = RE::NC; r.NG = RE::NG; r.NS = RE::NS;
     r.tile_rows = RE::TILE_ROWS;
     r.flops = RE::FLOPS; r.nnz = RE::NNZ; r.nnz_pm1 = RE::NNZ_PM1;
-    r.pair = RE::PAIR;
     r.sym = ST == 5;
     if constexpr (ST == 5) {
         for (int j = 0; j < RE::WT; ++j)

@@ -304,16 +304,9 @@ cudaError_t launch_qp_one(const QpArgs& a) {
     QpArgs b = a;
     b.nq_smem = a.nq < QP_SMEM_MAX / (int)(8 * TW) ? a.nq : QP_SMEM_MAX / (8 * TW);
     const size_t smem = sizeof(double) * (size_t)b.nq_smem * TW;
-    static size_t configured = 0;
-    static int occ = 0;
-    if (configured != smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, QP_THREADS, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-        configured = smem;
-    }
+    static std::atomic<uint64_t> cfg[MAX_DEVICES];   // per instantiation, per device (keyed on smem)
+    int occ = 1;
+    if (cudaError_t e = kernel_occupancy(kern, QP_THREADS, smem, cfg, &occ); e != cudaSuccess) return e;
     const int64_t nel = (a.tile_end - a.tile_begin) * TILE;
     constexpr int E = CC ? qp_ept<VT, F>() : 1;
     int64_t grid = (int64_t)a.num_sms * occ;

@@ -34,7 +34,9 @@ __global__ void __launch_bounds__(RED_THREADS) dot_kernel(const double* __restri
                                                           int64_t i0, int64_t i1, double* partials) {
     const double2* a2 = reinterpret_cast<const double2*>(a);
     const double2* b2 = reinterpret_cast<const double2*>(b);
-    const int64_t k0 = i0 / 2, k1 = (i1 + 1) / 2;
+    // whole pairs [k0, k1) lie below i1 (no read past element i1 - 1); an odd i1 leaves
+    // the tail element i1 - 1, added by one thread below
+    const int64_t k0 = i0 / 2, k1 = i1 / 2;
     const int64_t stride = (int64_t)gridDim.x * RED_THREADS;
     double s = 0.0;
     for (int64_t k = k0 + (int64_t)blockIdx.x * RED_THREADS + threadIdx.x; k < k1; k += VU * stride) {
@@ -52,6 +54,7 @@ __global__ void __launch_bounds__(RED_THREADS) dot_kernel(const double* __restri
             if (e + 1 >= i0 && e + 1 < i1) s = fma(va[j].y, vb[j].y, s);
         }
     }
+    if ((i1 & 1) && i1 - 1 >= i0 && blockIdx.x == 0 && threadIdx.x == 0) s = fma(a[i1 - 1], b[i1 - 1], s);
     s = block_sum(s);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }

@@ -151,9 +151,6 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
     const int64_t tile = eK / TILE;
     const int lane = (int)(eK % TILE);
     double* out = a.out + (size_t)tile * a.tile_rows * TILE + lane;
-    if (a.pair) {   // paired-lane WP layout: half-tiles of 16 columns [2 tile + lane/16][row][16]
-        out = a.out + ((size_t)(2 * tile + lane / 16) * a.tile_rows) * 16 + (lane % 16);
-    }
     double cconst[6] = {0, 0, 0, 0, 0, 0};
     if (direct) {
         double x[3] = {G.S[0], G.S[1], G.S[2]};
@@ -193,10 +190,6 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
         double ab[6];
         for (int c = 0; c < nc; ++c)
             ab[c] = direct ? adet * cconst[c] * a.sW[j] : a.scratch_a[(size_t)j * nb * nc + el * nc + c];
-        if (a.pair) {
-            out[(size_t)a.rowperm[j] * 16] = G.valid ? ab[0] : 0.0;
-            continue;
-        }
         if (!G.valid) {
             for (int c = 0; c < NC; ++c) out[(size_t)(j * NC + c) * TILE] = 0.0;
             continue;

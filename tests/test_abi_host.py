@@ -104,13 +104,13 @@ def test_mesh_argument_errors(args, code):
 
 
 def test_mesh_tile_count_limit():
-    """More than 2^30 element tiles per rank (tile_coord's 31-bit multiply-shift decode)
+    """2^31 or more element tiles per rank (tile_coord's 31-bit multiply-shift decode)
     is rejected at setup, before any allocation."""
     with pytest.raises(DogipError) as ei:
-        Mesh(3, 2048, 1, device=-1)
-    assert ei.value.code == -2 and "2^30" in str(ei.value)
-    m = Mesh(3, 2048, 1, rank=0, nranks=2, device=-1)      # half the layers: accepted
-    assert m.info["n_elem_local"] == 6 * 2048 ** 2 * 1024
+        Mesh(3, 2600, 1, device=-1)                          # 6 * 82 * 2600^2 = 3.3e9 tiles
+    assert ei.value.code == -2 and "2^31" in str(ei.value)
+    m = Mesh(3, 2600, 1, rank=0, nranks=2, device=-1)      # half the layers: accepted
+    assert m.info["n_elem_local"] == 6 * 2600 ** 2 * 1300
     m.close()
 
 
@@ -151,7 +151,7 @@ def test_header_constants_match_binding():
     binding's constants -- the ABI cannot drift silently."""
     text = open(HEADER).read()
     defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(DOGIP_[A-Z0-9_]+)\s+(-?\d+)", text)}
-    for name in ("DOGIP_STORE_FULL", "DOGIP_STORE_ISO", "DOGIP_STORE_GLOBAL", "DOGIP_STORE_PAIR",
+    for name in ("DOGIP_STORE_FULL", "DOGIP_STORE_ISO", "DOGIP_STORE_GLOBAL",
                  "DOGIP_STORE_QP", "DOGIP_STORE_SYM", "DOGIP_DIRICHLET_ZERO", "DOGIP_NO_EXCHANGE",
                  "DOGIP_CG_RESUME"):
         assert name in defs, name

@@ -21,7 +21,7 @@ from synth.configs import COEF_CONST, get_config
 G = 4096          # guard elements on each side (32 KB)
 SENT = 12345.0
 
-STORES = {0: (0, 2, 3, 4, 5), 1: (0, 1, 4)}      # DOGIP_STORE_* per form (WP, EL)
+STORES = {0: (0, 2, 4, 5), 1: (0, 1, 4)}      # DOGIP_STORE_* per form (WP, EL)
 
 
 def _cases():
@@ -64,7 +64,7 @@ def test_guard_bands(base, d, N, p):
                     assert any(k in str(e) for k in ("UNSUPPORTED", "INVALID", "BAD_COEFF")), e
                     continue
                 tag = f"form={form} store={store} coef={coef.kind}"
-                dir_ok = store != 3                    # PAIR: no Dirichlet elimination
+                dir_ok = True
                 y_big, y = _guarded(torch, n, SENT)
                 for dirichlet in (False, True) if dir_ok else (False,):
                     op.apply(u, y, dirichlet=dirichlet)

@@ -400,60 +400,6 @@ def test_global_storage_errors():
     assert ei.value.code == -10
 
 
-# Paired-lane WP layout (DOGIP_STORE_PAIR): ragged x-blocks of 16 (N = 5, 17, 33)
-PAIR_CASES = [(2, 17, 1), (2, 33, 2), (2, 9, 3), (2, 5, 4), (3, 3, 1), (3, 17, 2), (3, 5, 3), (3, 4, 4)]
-
-
-@pytest.mark.parametrize("d,N,p", PAIR_CASES)
-def test_pair_wp_storage_matches_oracle(d, N, p):
-    """DOGIP_STORE_PAIR: the same A_T^DoGIP values in the two-lanes-per-element
-    layout; y = A u element by element against the assembled A, the CG dot u^T A u,
-    and the exported weights equal the FULL layout's bit for bit."""
-    torch = _torch()
-    from paper_1710_09913_b200.api import Mesh, Operator
-    coef = TANH2 if d == 2 else TANH3
-    verts = jitter_verts(d, N)
-    m = Mesh(d, N, p, verts)
-    op = Operator(m, 0, coef, storage=3)
-    assert op.info["storage"] == 3
-    ed = oa.build(d, N, p, verts)
-    A = oa.assemble_csr(ed, 0, coef)
-    u = u_vector(ed.ndof, 0)
-    y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
-    assert relerr(y, A @ u) <= TOL
-    full = Operator(m, 0, coef, storage=0)
-    assert np.array_equal(op.export_weights(), full.export_weights())
-    # WP mass solve (no BC) through the paired kernel with the fused p.q
-    b = op.load_vector(1.0)
-    x = torch.zeros_like(b)
-    res = op.cg(b, x, rtol=1e-12)
-    bn, xn = b.cpu().numpy(), x.cpu().numpy()
-    assert res["status"] == "OK"
-    assert np.linalg.norm(bn - A @ xn) / np.linalg.norm(bn) <= 2e-12
-
-
-def test_pair_wp_c5_full_size_sampled():
-    torch = _torch()
-    from paper_1710_09913_b200.api import Mesh, Operator
-    c = get_config("C5")
-    coef, verts = c.coefficient(), c.vertices()
-    m = Mesh(3, c.N, c.p, verts)
-    op = Operator(m, 0, coef, storage=3)
-    u = c.u()
-    y = op.apply(torch.from_numpy(u).cuda()).cpu().numpy()
-    rows = np.unique(np.random.default_rng(17).integers(0, c.ndof, 30))
-    ref = oa.apply_rows_sampled(3, c.N, c.p, verts, 0, coef, u, rows)
-    assert np.abs(y[rows] - ref).max() / np.abs(y).max() <= TOL
-
-
-def test_pair_storage_errors():
-    from paper_1710_09913_b200.api import DogipError, Mesh, Operator
-    m = Mesh(3, 2, 2)
-    with pytest.raises(DogipError) as ei:
-        Operator(m, 1, TANH3, storage=3)
-    assert ei.value.code == -10
-
-
 # Quadrature-point matrix-free comparator (DOGIP_STORE_QP, "alternative approaches" P:61-75)
 QP_CASES = [(d, p, f) for d in (2, 3) for p in (1, 2, 3, 4) for f in (0, 1)]
 
@@ -653,7 +599,7 @@ def test_nccl_single_rank_communicator(d, N, p, form, storage):
 
 
 # ------------------------------------------------------------------ degenerate sizes
-STORES_BY_FORM = {0: (0, 2, 3, 4, 5), 1: (0, 1, 4)}
+STORES_BY_FORM = {0: (0, 2, 4, 5), 1: (0, 1, 4)}
 
 
 @pytest.mark.gpu
@@ -678,11 +624,6 @@ def test_smallest_meshes_every_storage(d, p, form, N):
         op = Operator(m, form, coef, storage=store)
         y = op.apply(ut).cpu().numpy()
         assert relerr(y, A @ u) <= TOL, store
-        if store == 3:       # the paired-lane layout has no Dirichlet elimination
-            with pytest.raises(RuntimeError, match="PAIR"):
-                op.apply(ut, dirichlet=True)
-            op.close()
-            continue
         yd = op.apply(ut, dirichlet=True).cpu().numpy()
         assert relerr(yd, AD @ u) <= TOL, store
         b = torch.zeros_like(ut)
@@ -715,25 +656,23 @@ def test_every_storage_every_entry_point(d, p, form):
     ut = torch.from_numpy(u).cuda()
     for store in STORES_BY_FORM[form]:
         op = Operator(m, form, coef, storage=store)
-        dirs = (False,) if store == 3 else (False, True)
-        for dirichlet in dirs:
+        for dirichlet in (False, True):
             ref = (AD if dirichlet else A) @ u
             assert relerr(op.apply(ut, dirichlet=dirichlet).cpu().numpy(), ref) <= TOL, (store, dirichlet)
             assert relerr(op.apply_host(u, dirichlet=dirichlet), ref) <= TOL, (store, dirichlet, "host")
-        if store != 3:
-            bt = torch.from_numpy(b).cuda()
-            for graph in (True, False):
-                x = torch.zeros_like(bt)
+        bt = torch.from_numpy(b).cuda()
+        for graph in (True, False):
+            x = torch.zeros_like(bt)
+            if not graph:
+                import os
+                os.environ["DOGIP_CG_NO_GRAPH"] = "1"
+            try:
+                r = op.cg(bt, x, rtol=1e-300, maxit=6, dirichlet=True)
+            finally:
                 if not graph:
-                    import os
-                    os.environ["DOGIP_CG_NO_GRAPH"] = "1"
-                try:
-                    r = op.cg(bt, x, rtol=1e-300, maxit=6, dirichlet=True)
-                finally:
-                    if not graph:
-                        del os.environ["DOGIP_CG_NO_GRAPH"]
-                assert r["iters"] == 6
-                assert relerr(x.cpu().numpy(), x_ref6) <= 1e-9, (store, graph)
+                    del os.environ["DOGIP_CG_NO_GRAPH"]
+            assert r["iters"] == 6
+            assert relerr(x.cpu().numpy(), x_ref6) <= 1e-9, (store, graph)
         op.close()
     m.close()
 
@@ -761,7 +700,7 @@ def test_slab_partials_every_storage(d, N, p, form, nr):
             continue
         opg = Operator(mg, form, coef, storage=store)
         ops = [Operator(m, form, coef, storage=store) for m in meshes]
-        for dirichlet in ((False,) if store == 3 else (False, True)):
+        for dirichlet in (False, True):
             y_glob = opg.apply(ug, dirichlet=dirichlet).cpu().numpy()
             acc = np.zeros_like(u)
             for m, op in zip(meshes, ops):
