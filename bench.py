@@ -32,6 +32,12 @@ import sys
 import threading
 import time
 
+if "--impl" in sys.argv and "reference" in sys.argv or "--cpu-baseline-only" in sys.argv:
+    # oracle processes: one BLAS thread per worker process (the pool supplies the cores),
+    # and no BLAS thread pool alive when the workers are forked
+    for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[_v] = "1"
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -131,7 +137,7 @@ def oracle_sample_apply(cfg, n_cells: int, seed_offset: int = 0):
     M = N + 1
     vids = np.unique(elems)
     vlat = np.stack([(vids // M ** a) % M for a in range(d)], axis=1)
-    verts = cfg.vertices()
+    verts = _ORACLE_CACHE.setdefault(cfg.name + "v", cfg.vertices())
     X = vlat / N if verts is None else verts[vids]
     remap = np.full(vids.max() + 1, -1, dtype=np.int64)
     remap[vids] = np.arange(vids.size)
@@ -151,6 +157,83 @@ def oracle_sample_apply(cfg, n_cells: int, seed_offset: int = 0):
 
 
 _ORACLE_CACHE: dict = {}
+_POOL_CFG = None
+
+
+def _pool_task(args):
+    n_cells, offset = args
+    return oracle_sample_apply(_POOL_CFG, n_cells, offset)
+
+
+def _cores() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def _blas_vendor() -> str:
+    try:
+        from threadpoolctl import threadpool_info
+        libs = [f"{i.get('internal_api')} {i.get('version')}" for i in threadpool_info() if i.get("user_api") == "blas"]
+        return ", ".join(libs) or "none loaded"
+    except Exception as e:   # noqa: BLE001
+        return f"unknown ({e})"
+
+
+def oracle_parallel_sample(cfg, target_s: float, offset0: int = 0):
+    """The oracle as it stands, on every host core: one worker process per core, each
+    running the element route on its own block of consecutive cells (disjoint blocks),
+    about target_s seconds of work per worker.  Returns (elements, wall seconds, cores,
+    per-worker elements)."""
+    global _POOL_CFG
+    import multiprocessing as mp
+    cores = _cores()
+    oracle_sample_apply(cfg, 8)                                    # imports, caches (inherited by fork)
+    ne, t = oracle_sample_apply(cfg, 128)
+    per_cell = t / (128)
+    n_cells = int(max(16, min(cfg.N ** cfg.d // max(1, cores), target_s / per_cell)))
+    _POOL_CFG = cfg
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_pool_task, [(n_cells, offset0 * cores + k) for k in range(cores)], chunksize=1)
+        wall = time.perf_counter() - t0
+    return sum(r[0] for r in res), wall, cores, res[0][0]
+
+
+def oracle_vector_ops_s(ndof: int) -> float:
+    """NumPy time of CG's vector work per iteration on full-length vectors (2 dots,
+    3 axpy-type updates: oracle/cg.py), single process."""
+    rng = np.random.default_rng(0)
+    x, r, p, q = (rng.standard_normal(ndof) for _ in range(4))
+    t0 = time.perf_counter()
+    pq = float(p @ q)
+    alpha = 1e-3 / max(abs(pq), 1e-300)
+    x = x + alpha * p
+    r = r - alpha * q
+    rr = float(r @ r)
+    p = r + (rr * 1e-3) * p
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, target_s: float = 8.0) -> dict:
+    """Oracle throughput in the metric's unit on a bounded element sample, all host cores."""
+    ne, wall, cores, per = oracle_parallel_sample(cfg, target_s)
+    frac = ne / cfg.n_elem
+    gdofs = cfg.ndof * frac / wall / 1e9
+    t_apply_full = wall / frac                                       # extrapolated to the whole mesh
+    t_vec = oracle_vector_ops_s(cfg.ndof) if cfg.ndof <= 1e8 else None
+    return {"value": gdofs, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
+            "blas": _blas_vendor(),
+            "sample": f"oracle element route (NumPy einsum per element chunk), {cores} worker processes x "
+                      f"{per} elements of consecutive cells = {ne} of {cfg.n_elem} elements of {cfg.name}; "
+                      f"GDoF/s = ndof * sampled fraction / wall time",
+            "seconds": wall,
+            "cg_s_per_iter": (t_apply_full + t_vec) if t_vec is not None else None,
+            "cg_s_per_iter_how": "extrapolated: element-route apply time of the sample scaled to the whole mesh "
+                                 "(same cores) + measured NumPy vector work of one iteration on full-length "
+                                 "vectors (2 dots, 3 updates, one process)"}
 
 
 def _cpu_model() -> str:
@@ -164,47 +247,44 @@ def _cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(cfg, target_s: float = 12.0) -> dict:
-    """Oracle throughput in the metric's unit on a bounded element sample."""
-    oracle_sample_apply(cfg, 8)                                     # warm caches / imports
-    ne, t = oracle_sample_apply(cfg, 256)
-    per_elem = t / ne
-    n_cells = int(max(256, min(cfg.N ** cfg.d, target_s / per_elem / (2 if cfg.d == 2 else 6))))
-    ne, t = oracle_sample_apply(cfg, n_cells, 1)
-    frac = ne / cfg.n_elem
-    gdofs = cfg.ndof * frac / t / 1e9
-    return {"value": gdofs, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu_model": _cpu_model(),
-            "sample": f"oracle element route (NumPy, single-threaded einsum) over {ne} of {cfg.n_elem} "
-                      f"elements ({n_cells} cells) of {cfg.name}; GDoF/s = ndof * sampled fraction / time",
-            "seconds": t}
+def run_cpu_baseline_only(args, cfg) -> None:
+    print(json.dumps(cpu_baseline(cfg)), flush=True)
+
+
+def cpu_baseline_subprocess(cfg_name: str) -> dict:
+    """cpu_baseline in a fresh process (no CUDA context, no torch threads: safe to fork)."""
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-only", "--config", cfg_name],
+                       capture_output=True, text=True, timeout=900)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    if r.returncode != 0 or not lines:
+        return {"value": None, "unit": UNIT, "cores": _cores(), "kind": "oracle",
+                "sample": "failed: " + r.stderr[-300:]}
+    return json.loads(lines[-1])
 
 
 def run_reference(args, cfg) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    _ = oracle_sample_apply(cfg, 8)
-    ne, t = oracle_sample_apply(cfg, 256)
-    per_elem = t / ne
     per_step_target = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
-    n_cells = int(max(64, per_step_target / per_elem / (2 if cfg.d == 2 else 6)))
     for w in range(args.warmup):
-        oracle_sample_apply(cfg, n_cells, w)
-    times, nes = [], []
+        oracle_parallel_sample(cfg, per_step_target, w)
+    walls, nes = [], []
+    cores, per = _cores(), 0
     for k in range(args.steps):
-        ne, t = oracle_sample_apply(cfg, n_cells, args.warmup + k)
-        times.append(t)
+        ne, wall, cores, per = oracle_parallel_sample(cfg, per_step_target, args.warmup + k)
+        walls.append(wall)
         nes.append(ne)
-    tot = sum(times)
+    tot = sum(walls)
     frac = sum(nes) / cfg.n_elem
     value = cfg.ndof * frac / tot / 1e9
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": _config_dict(cfg, args.gpus),
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "blas": _blas_vendor(),
                             "sample": f"each step: oracle element-route apply over {nes[0]} elements "
-                                      f"({n_cells} cells) of {cfg.name}"},
+                                      f"({cores} processes x {per} elements of consecutive cells) of {cfg.name}"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -219,6 +299,76 @@ def _config_dict(cfg, n_gpus):
 
 
 # ----------------------------------------------------------------- product arm
+SECONDARY = [("C1", "full"), ("C2p1", "full"), ("C2p2", "full"), ("C2p3", "full"), ("C2p4", "full"),
+             ("C2p4", "iso"), ("C3", "full"), ("C4", "iso"), ("C5", "full"), ("C5", "sym"), ("C5", "global")]
+STORE_CODE = {"full": 0, "iso": 1, "global": 2, "sym": 5}
+
+
+def alg_bytes(oinfo: dict, n_elem: int, ndof: int) -> int:
+    """Algorithmic bytes of one apply: streamed weights of real elements
+    + u read once + y written once (GLOBAL: the W-lattice vector read once)."""
+    st = oinfo["storage"]
+    if st == 2:
+        return int(oinfo["weight_bytes"]) + 16 * ndof
+    n_w = oinfo["W_T"] + oinfo["n_c"] if st == 1 else oinfo["W_T"] * oinfo["n_c"]
+    return 8 * n_w * n_elem + 16 * ndof
+
+
+def secondary_configs(args, stream) -> list:
+    """Every BASELINE.json config on this GPU, each apply timed alone with the L2 flushed
+    before it (a 256 MB write; median of K), plus CG ms per iteration (fixed count, warm)."""
+    import torch
+    from paper_1710_09913_b200.api import Mesh, Operator
+    from synth.configs import get_config
+    peak, _ = _measured_peaks()
+    flush = torch.empty(32 * 2 ** 20, dtype=torch.float64, device="cuda")
+    K = max(5, min(args.steps, 20))
+    rows = []
+    for name, storage in SECONDARY:
+        c = get_config(name)
+        form = c.forms[-1]
+        dirichlet = form == 1
+        t0 = time.perf_counter()
+        m = Mesh(c.d, c.N, c.p, c.vertices())
+        op = Operator(m, form, c.coefficient(), storage=STORE_CODE[storage])
+        oi = op.info
+        u = torch.from_numpy(c.u()).cuda()
+        y = torch.empty_like(u)
+        for _ in range(3):
+            op.apply(u, y, dirichlet=dirichlet)
+        ts = []
+        for k in range(K):
+            flush.fill_(float(k))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            op.apply(u, y, dirichlet=dirichlet)
+            e1.record(stream)
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        t = float(np.median(ts))
+        b = op.load_vector(1.0, dirichlet=dirichlet)
+        x = torch.zeros_like(b)
+        op.cg(b, x, maxit=-3, dirichlet=dirichlet)
+        r = op.cg(b, x, maxit=-K, dirichlet=dirichlet, resume=True)
+        ab = alg_bytes(oi, c.n_elem, c.ndof)
+        fl = oi["flops_per_elem"] * c.n_elem
+        rows.append({"config": name, "storage": storage, "form": "EL" if form == 1 else "WP", "d": c.d, "N": c.N,
+                     "p": c.p, "ndof": c.ndof, "n_elem": c.n_elem, "dirichlet": dirichlet,
+                     "apply_ms": t * 1e3, "apply_ms_min": min(ts) * 1e3, "GDoF_s": c.ndof / t / 1e9,
+                     "alg_bytes": ab, "achieved_GBs": ab / t / 1e9, "frac_measured_hbm": ab / t / 1e9 / peak,
+                     "frac_8TBs": ab / t / 8e12, "fp64_TFs": fl / t / 1e12,
+                     "fp64_frac_measured_dfma": fl / t / 1e12 / FP64_PEAK_TFLOPS,
+                     "cg_ms_per_iter": r["seconds"] / K * 1e3, "weights_ms": oi["weights_ms"],
+                     "l2": "flushed (256 MB write) before each timed apply; CG iterations back to back",
+                     "setup_s": time.perf_counter() - t0})
+        op.close()
+        m.close()
+        del u, y, b, x
+        torch.cuda.empty_cache()
+    del flush
+    return rows
+
+
 def run_product(args, cfg) -> None:
     import torch
     import torch.distributed as dist
@@ -280,11 +430,10 @@ def run_product(args, cfg) -> None:
 
     # algorithmic bytes of one apply on this rank: streamed weights of
     # real elements + u read once + y written once
-    n_w = oinfo["W_T"] + oinfo["n_c"] if storage == 1 else oinfo["W_T"] * oinfo["n_c"]
-    alg_bytes = 8 * n_w * info["n_elem_local"] + 16 * info["ndof_local"]
+    alg_b = alg_bytes(oinfo, info["n_elem_local"], info["ndof_local"])
     flops_apply = oinfo["flops_per_elem"] * info["n_elem_local"]
     peak, peak_src = _measured_peaks()
-    achieved = alg_bytes / t_apply / 1e9
+    achieved = alg_b / t_apply / 1e9
 
     # e2e: host buffers through the public API (dogip_apply_host), copies inside
     u_host = torch.from_numpy(cfg.u()[info["dof_offset"]:info["dof_offset"] + info["ndof_local"]].copy()).pin_memory()
@@ -326,35 +475,11 @@ def run_product(args, cfg) -> None:
         dist.all_reduce(t_cg, op=dist.ReduceOp.MAX)
     t_cg_e2e = t_cg.item()
 
-    # secondary (not the headline): the isotropic compressed storage of the corollary
-    # P:411-428 on the same workload -- FP64-bound instead of HBM-bound
-    iso = None
-    if form == 1 and storage == 0 and coef.isotropic and not args.no_variants:
-        op.close()                      # free the full weights first (21 GB at N=1)
-        torch.cuda.empty_cache()
-        op2 = Operator(mesh, form, coef, storage=1)
-        y2 = torch.empty_like(b)
-        for _ in range(3):
-            op2.apply(b, y2, dirichlet=dirichlet)
-        barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record(stream)
-        for _ in range(args.steps):
-            op2.apply(b, y2, dirichlet=dirichlet)
-        g1.record(stream)
-        barrier()
-        ti = torch.tensor([g0.elapsed_time(g1) * 1e-3 / args.steps], dtype=torch.float64, device="cuda")
-        if dist_on:
-            dist.all_reduce(ti, op=dist.ReduceOp.MAX)
-        oi2 = op2.info
-        t_iso = ti.item()
-        iso = {"storage": "iso (a_{T,j} and G_T = R^-1 R^-T, P:411-428)", "apply_ms": t_iso * 1e3,
-               "value": info["ndof_global"] / t_iso / 1e9, "unit": UNIT,
-               "bound": "fp64", "fp64_tflops": oi2["flops_per_elem"] * info["n_elem_local"] / t_iso / 1e12,
-               "fp64_frac_of_measured_dfma": oi2["flops_per_elem"] * info["n_elem_local"] / t_iso / 1e12 / FP64_PEAK_TFLOPS,
-               "weights_ms": oi2["weights_ms"],
-               "alg_bytes_per_launch": 8 * (oi2["W_T"] + oi2["n_c"]) * info["n_elem_local"] + 16 * info["ndof_local"]}
-        op2.close()
+    op.close()                          # free the headline weights (21 GB at N=1) before the configs block
+    torch.cuda.empty_cache()
+    configs = None
+    if world == 1 and not args.no_variants:
+        configs = secondary_configs(args, stream)
     nbytes_vec = 8 * info["ndof_local"]
     tot_vec = torch.tensor([nbytes_vec], dtype=torch.float64, device="cuda")
     if dist_on:
@@ -372,7 +497,10 @@ def run_product(args, cfg) -> None:
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                             "frac": achieved / peak, "traffic": _traffic_from_profiles(cfg.name, world),
                             "kernel": "DoGIP apply (memset y + apply_kernel + Dirichlet fix-up), rank 0",
-                            "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                            "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per apply launch from "
+                                              "the committed ncu --set full capture (profiles/ncu_traffic.json), "
+                                              "not measured in this run",
+                            "alg_bytes_per_launch": alg_b, "peak_source": peak_src,
                             "frac_of_8TBs": achieved / 8000.0,
                             "fp64_tflops": flops_apply / t_apply / 1e12,
                             "fp64_frac_of_measured_dfma": flops_apply / t_apply / 1e12 / FP64_PEAK_TFLOPS},
@@ -388,10 +516,10 @@ def run_product(args, cfg) -> None:
                                  "b in from / x out to pinned host memory once per run (bytes amortised per step)"},
                "gpu_launches": int(launches),
                "clocks": clocks}
-        if iso:
-            out["variants"] = {"iso": iso}
+        if configs:
+            out["configs"] = configs
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(cfg)
+            out["cpu_baseline"] = cpu_baseline_subprocess(cfg.name)
         print(json.dumps(out), flush=True)
     if dist_on:
         dist.barrier()
@@ -415,9 +543,29 @@ def main():
                     help="weight storage: full (P:281 / P:443), iso = EL isotropic compression of "
                          "the corollary P:411-428 (a_{T,j} R^-1 R^-T), sym = WP symmetry-adapted "
                          "(DOGIP_STORE_SYM, e.g. --config C5 --storage sym)")
+    ap.add_argument("--cpu-baseline-only", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     from synth.configs import get_config
     cfg = get_config(args.config)
+    if args.cpu_baseline_only:
+        run_cpu_baseline_only(args, cfg)
+        return
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None and int(world_env) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world_env} but --gpus {args.gpus}; launch one rank per requested GPU")
+    if world_env is None and args.gpus > 1 and args.impl == "product":
+        # not under torchrun: launch the N ranks ourselves (one process per GPU, NCCL)
+        import torch
+        n_vis = torch.cuda.device_count()
+        if n_vis < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n_vis}")
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -125,6 +125,15 @@ extern "C" {
 
 typedef struct dogip_mesh_s* dogip_mesh;
 typedef struct dogip_op_s*   dogip_op;
+typedef struct dogip_loopback_s* dogip_loopback;
+
+/* ---- communicator kinds (dogip_mesh_setup_ex) ---------------------------- */
+#define DOGIP_COMM_NONE      0  /* single rank, or partial sums only (DOGIP_NO_EXCHANGE)     */
+#define DOGIP_COMM_NCCL      1  /* comm_arg = 128-byte ncclUniqueId: one process per GPU     */
+#define DOGIP_COMM_LOOPBACK  2  /* comm_arg = dogip_loopback: every rank in THIS process, one
+                                   host thread per rank, same device; planes and scalars are
+                                   moved with cudaMemcpyAsync, host threads rendezvous per
+                                   collective (tests of the multi-rank path on one GPU)     */
 
 typedef struct {
     int      d, p, rank, nranks;
@@ -197,6 +206,23 @@ const char* dogip_last_error(void);
 int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices, int rank, int nranks,
                      const void* nccl_id, int device, dogip_mesh* out);
 
+/*
+ * dogip_mesh_setup_ex -- dogip_mesh_setup with an explicit communicator kind
+ * (DOGIP_COMM_*).  dogip_mesh_setup(..., nccl_id, ...) is dogip_mesh_setup_ex with
+ * DOGIP_COMM_NCCL when nccl_id != NULL, else DOGIP_COMM_NONE.  With DOGIP_COMM_LOOPBACK
+ * every later collective call (apply / load vector / CG / GLOBAL weights) of each rank
+ * must be made from that rank's own host thread, concurrently with the other ranks.
+ * Errors: as dogip_mesh_setup; E_INVALID_ARG (unknown kind, missing comm_arg, loopback
+ * group of another device or size).
+ */
+int dogip_mesh_setup_ex(int d, int64_t N, int p, const double* vertices, int rank, int nranks,
+                        int comm_kind, const void* comm_arg, int device, dogip_mesh* out);
+
+/* In-process loopback group of nranks ranks on `device` (DOGIP_COMM_LOOPBACK).  Destroy
+ * after every mesh using it (else E_INVALID_ARG). */
+int dogip_loopback_create(int nranks, int device, dogip_loopback* out);
+int dogip_loopback_destroy(dogip_loopback group);
+
 int dogip_mesh_info(dogip_mesh mesh, dogip_mesh_info_t* out);
 
 /* Rank 0 creates the 128-byte ncclUniqueId passed to dogip_mesh_setup by
@@ -238,7 +264,9 @@ int dogip_op_info(dogip_op op, dogip_op_info_t* out);
  * consistent across ranks; y: device, ndof_local, overwritten; with nranks > 1
  * y's interface planes are summed over both owners on return (NCCL exchange
  * overlapped with interior elements) unless DOGIP_NO_EXCHANGE.  u and y must
- * not alias.  Asynchronous on `stream`.  Errors: E_INVALID_ARG, E_CUDA, E_NCCL.
+ * not alias.  Asynchronous on `stream`.  Errors: E_INVALID_ARG, E_CUDA, E_NCCL
+ * (an asynchronous communicator failure of an earlier call is reported here and the
+ * communicator aborted).
  */
 int dogip_apply(dogip_op op, const double* u, double* y, unsigned flags, void* stream);
 
@@ -269,11 +297,17 @@ int dogip_load_vector(dogip_op op, double f, double* b, unsigned flags, void* st
  * iterations (maxit < 0: run exactly -maxit iterations, no convergence test --
  * benchmarking).  b, x: device, ndof_local.  Dots run over owned DoFs and are
  * all-reduced.  Synchronises `stream`.  Returns DOGIP_OK, DOGIP_NOT_CONVERGED
- * or DOGIP_E_BREAKDOWN (also in res->status).  Single rank, maxit > 0: the
- * iterations run as one CUDA graph (conditional WHILE node around one iteration,
- * device-side stopping test, no host round trip per iteration; built once per
- * (x, flags, rtol, maxit, stream) and cached in the op, outside the timed
- * res->seconds); environment DOGIP_CG_NO_GRAPH=1 selects the host-driven loop.
+ * or DOGIP_E_BREAKDOWN (also in res->status; on breakdown x holds the last iterate).
+ * The stopping test runs on the device after every iteration (no host round trip
+ * per iteration).  Single rank, maxit > 0: the iterations run as one CUDA graph
+ * (conditional WHILE node around one iteration; built once per (x, flags, rtol,
+ * maxit, stream) and cached in the op, outside the timed res->seconds).  Otherwise
+ * (several ranks, or DOGIP_CG_NO_GRAPH=1) batches of DOGIP_CG_BATCH (default 32)
+ * iterations are enqueued at once and the host reads the device's done flag once
+ * per batch; iterations enqueued after the stop are no-ops (the apply kernel returns
+ * at once).  With a communicator every wait polls its asynchronous error state: a
+ * dead peer or no progress within DOGIP_COMM_TIMEOUT_S seconds (default 600) aborts
+ * the communicator and returns E_NCCL.
  */
 int dogip_cg(dogip_op op, const double* b, double* x, double rtol, int maxit, unsigned flags,
              void* stream, dogip_cg_result* res);
@@ -308,6 +342,12 @@ int dogip_export_weights(dogip_op op, double* host_out, int64_t cap);
 
 /* l_T of this rank: (n_elem_local, V_T) LOCAL DoF ids, canonical element order. */
 int dogip_export_dofmap(dogip_mesh mesh, int64_t* host_out, int64_t cap);
+
+/* TEST HOOK (negative control of the parity tests, not for production): adds `delta`
+ * to the stored weight A_{T,j} component c (canonical order of dogip_export_weights) of
+ * local element `elem`, in place on the device.  DOGIP_STORE_FULL only (else
+ * E_INVALID_ARG); E_INVALID_SIZE for an index out of range.  Synchronous. */
+int dogip_test_perturb_weight(dogip_op op, int64_t elem, int j, int c, double delta);
 
 void dogip_op_destroy(dogip_op op);
 void dogip_mesh_destroy(dogip_mesh mesh);

@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libdogip.so")
 DOGIP_WP, DOGIP_EL = 0, 1
 DOGIP_STORE_FULL, DOGIP_STORE_ISO, DOGIP_STORE_GLOBAL, DOGIP_STORE_QP, DOGIP_STORE_SYM = 0, 1, 2, 4, 5
 DOGIP_DIRICHLET_ZERO, DOGIP_NO_EXCHANGE, DOGIP_CG_RESUME = 1, 2, 4
+DOGIP_COMM_NONE, DOGIP_COMM_NCCL, DOGIP_COMM_LOOPBACK = 0, 1, 2
 STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "E_INVALID_DIM", -2: "E_INVALID_SIZE",
           -3: "E_UNSUPPORTED_ORDER", -4: "E_DEGENERATE_ELEMENT", -5: "E_BAD_COEFF", -6: "E_OOM",
           -7: "E_CUDA", -8: "E_NCCL", -9: "E_BREAKDOWN", -10: "E_INVALID_ARG"}
@@ -54,6 +55,10 @@ SIGNATURES = [
     ("dogip_slab_range", C.c_int, [C.c_int64, C.c_int, C.c_int, c_i64p, c_i64p]),
     ("dogip_mesh_setup", C.c_int, [C.c_int, C.c_int64, C.c_int, c_dp, C.c_int, C.c_int, C.c_void_p,
                                    C.c_int, C.POINTER(C.c_void_p)]),
+    ("dogip_mesh_setup_ex", C.c_int, [C.c_int, C.c_int64, C.c_int, c_dp, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                      C.c_int, C.POINTER(C.c_void_p)]),
+    ("dogip_loopback_create", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    ("dogip_loopback_destroy", C.c_int, [C.c_void_p]),
     ("dogip_mesh_info", C.c_int, [C.c_void_p, C.POINTER(MeshInfo)]),
     ("dogip_weights", C.c_int, [C.c_void_p, C.c_int, C.POINTER(Coeff), C.c_int, C.c_void_p,
                                 C.POINTER(C.c_void_p)]),
@@ -72,6 +77,7 @@ SIGNATURES = [
     ("dogip_quadrature", C.c_int, [C.c_int, C.c_int, c_dp, c_dp, C.c_int64]),
     ("dogip_export_weights", C.c_int, [C.c_void_p, c_dp, C.c_int64]),
     ("dogip_export_dofmap", C.c_int, [C.c_void_p, c_i64p, C.c_int64]),
+    ("dogip_test_perturb_weight", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_double]),
     ("dogip_op_destroy", None, [C.c_void_p]),
     ("dogip_mesh_destroy", None, [C.c_void_p]),
 ]

@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from ._lib import DOGIP_DIRICHLET_ZERO, DOGIP_EL, DOGIP_NO_EXCHANGE, DOGIP_WP, DogipError, check, load
 
-__all__ = ["Mesh", "Operator", "CoeffSpec", "DOGIP_WP", "DOGIP_EL", "DogipError",
+__all__ = ["Mesh", "Operator", "LoopbackGroup", "CoeffSpec", "DOGIP_WP", "DOGIP_EL", "DogipError",
            "reference_table", "reference_nnz", "quadrature", "slab_range", "nccl_unique_id"]
 
 
@@ -99,17 +99,48 @@ def quadrature(d: int, n1d: int):
     return pts, wts
 
 
+class LoopbackGroup:
+    """In-process communicator of `nranks` ranks on one device (DOGIP_COMM_LOOPBACK): each
+    rank's mesh is driven from its own host thread; the library moves interface planes and
+    CG scalars between the ranks with cudaMemcpyAsync (tests of the multi-rank path)."""
+
+    def __init__(self, nranks: int, device: int = 0):
+        self._lib = load()
+        h = C.c_void_p()
+        check(self._lib.dogip_loopback_create(int(nranks), int(device), C.byref(h)))
+        self.handle, self.nranks, self.device = h, nranks, device
+
+    def close(self):
+        if getattr(self, "handle", None):
+            check(self._lib.dogip_loopback_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Mesh:
-    """Structured simplex mesh M_N + P_p DoF plan (+ slab partition, NCCL comm)."""
+    """Structured simplex mesh M_N + P_p DoF plan (+ slab partition, NCCL or loopback comm)."""
 
     def __init__(self, d: int, N: int, p: int, vertices: Optional[np.ndarray] = None, rank: int = 0,
-                 nranks: int = 1, nccl_id: Optional[bytes] = None, device: int = 0):
+                 nranks: int = 1, nccl_id: Optional[bytes] = None, device: int = 0,
+                 loopback: Optional[LoopbackGroup] = None):
         lib = load()
         self._lib = lib
         self._verts = None if vertices is None else np.ascontiguousarray(vertices, dtype=np.float64)
         h = C.c_void_p()
-        idbuf = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
-        check(lib.dogip_mesh_setup(d, N, p, _dptr(self._verts), rank, nranks, idbuf, device, C.byref(h)))
+        if loopback is not None:
+            if nccl_id is not None:
+                raise ValueError("pass either nccl_id or loopback")
+            self._group = loopback          # the group must outlive the mesh
+            check(lib.dogip_mesh_setup_ex(d, N, p, _dptr(self._verts), rank, nranks, _lib.DOGIP_COMM_LOOPBACK,
+                                          loopback.handle, device, C.byref(h)))
+        else:
+            idbuf = None if nccl_id is None else C.create_string_buffer(nccl_id, 128)
+            check(lib.dogip_mesh_setup(d, N, p, _dptr(self._verts), rank, nranks, idbuf, device, C.byref(h)))
         self.handle = h
         self.device = device
         info = _lib.MeshInfo()
@@ -224,6 +255,10 @@ class Operator:
         out = np.empty((self.mesh.info["n_elem_local"], i["W_T"], i["n_c"]))
         check(self._lib.dogip_export_weights(self.handle, _dptr(out), out.size))
         return out
+
+    def _test_perturb_weight(self, elem: int, j: int, c: int, delta: float):
+        """Test hook (negative control): A_{T,j}[c] += delta on the device (FULL storage)."""
+        check(self._lib.dogip_test_perturb_weight(self.handle, int(elem), int(j), int(c), float(delta)))
 
     def close(self):
         if getattr(self, "handle", None):

@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
+#include <memory>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -39,6 +42,12 @@ static int fail(int code, const std::string& msg) {
         if (r_ != ncclSuccess)                                                              \
             return fail(DOGIP_E_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)); \
     } while (0)
+// a collective of the mesh's communicator (comm.hpp); failures carry the backend's message
+#define CM(m, call)                                           \
+    do {                                                      \
+        int rc_ = (call);                                     \
+        if (rc_) return fail(rc_, (m)->comm->err);            \
+    } while (0)
 #define RET(call)                     \
     do {                              \
         int rc_ = (call);             \
@@ -53,7 +62,7 @@ struct dogip_mesh_s {
     ApplyTables tab{};
     RefInfo ref{};          // V-side layout (form independent)
     double* d_verts = nullptr;
-    ncclComm_t comm = nullptr;
+    Comm* comm = nullptr;     // NCCL or in-process loopback (owned); null: single rank / partial sums
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
     double* rbuf = nullptr;   // 2 planes: from rank-1, from rank+1
@@ -85,7 +94,6 @@ struct dogip_op_s {
     // graph-captured CG loop (single rank): conditional WHILE node around one iteration
     cudaGraph_t cg_graph = nullptr;
     cudaGraphExec_t cg_exec = nullptr;
-    int* cg_it = nullptr;
     cudaStream_t cap_stream = nullptr;   // capture stream (the legacy default stream cannot capture)
     struct { const double* x = nullptr; unsigned flags = 0; double rtol = 0.0; int maxit = 0; cudaStream_t st = nullptr; } cg_key;
     // pipelined host-buffer apply: copy-in / copy-out streams, one event pair per chunk
@@ -143,9 +151,56 @@ extern "C" int dogip_nccl_unique_id(void* out128) {
 }
 
 // ------------------------------------------------------------------ mesh
+// ------------------------------------------------------------------ loopback groups
+struct dogip_loopback_s {
+    LoopbackGroup g;
+};
+
+extern "C" int dogip_loopback_create(int nranks, int device, dogip_loopback* out) {
+    if (!out) return fail(DOGIP_E_INVALID_ARG, "null output handle");
+    *out = nullptr;
+    if (nranks < 1) return fail(DOGIP_E_INVALID_SIZE, "loopback group needs nranks >= 1");
+    DeviceGuard dg(device);
+    auto* L = new dogip_loopback_s();
+    L->g.nranks = nranks;
+    L->g.device = device;
+    L->g.sendbox.resize((size_t)nranks * nranks);
+    L->g.donebox.resize((size_t)nranks * nranks);
+    L->g.arbox.resize(nranks);
+    if (cudaMalloc(&L->g.slots, sizeof(double) * 2 * nranks * LoopbackGroup::SLOT) != cudaSuccess) {
+        delete L;
+        return fail(DOGIP_E_OOM, "loopback scratch");
+    }
+    *out = L;
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_loopback_destroy(dogip_loopback L) {
+    if (!L) return DOGIP_OK;
+    {
+        std::lock_guard<std::mutex> lk(L->g.mu);
+        if (L->g.members > 0) return fail(DOGIP_E_INVALID_ARG, "loopback group still has meshes attached");
+    }
+    DeviceGuard dg(L->g.device);
+    cudaFree(L->g.slots);
+    delete L;
+    return DOGIP_OK;
+}
+
 extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices, int rank, int nranks,
                                 const void* nccl_id, int device, dogip_mesh* out) {
+    return dogip_mesh_setup_ex(d, N, p, vertices, rank, nranks, nccl_id ? DOGIP_COMM_NCCL : DOGIP_COMM_NONE,
+                               nccl_id, device, out);
+}
+
+extern "C" int dogip_mesh_setup_ex(int d, int64_t N, int p, const double* vertices, int rank, int nranks,
+                                   int comm_kind, const void* comm_arg, int device, dogip_mesh* out) {
     if (!out) return fail(DOGIP_E_INVALID_ARG, "null output handle");
+    if (comm_kind != DOGIP_COMM_NONE && comm_kind != DOGIP_COMM_NCCL && comm_kind != DOGIP_COMM_LOOPBACK)
+        return fail(DOGIP_E_INVALID_ARG, "unknown communicator kind");
+    if (comm_kind != DOGIP_COMM_NONE && !comm_arg) return fail(DOGIP_E_INVALID_ARG, "communicator argument missing");
+    if (comm_kind == DOGIP_COMM_LOOPBACK && device != static_cast<const dogip_loopback_s*>(comm_arg)->g.device)
+        return fail(DOGIP_E_INVALID_ARG, "loopback ranks must run on the group's device");
     *out = nullptr;
     if (d != 2 && d != 3) return fail(DOGIP_E_INVALID_DIM, "invalid-dimension: d must be 2 or 3");
     if (N < 1) return fail(DOGIP_E_INVALID_SIZE, "invalid-size: N must be >= 1");
@@ -220,13 +275,21 @@ extern "C" int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices,
         if (e == cudaSuccess) e = cudaMemcpy(m->d_verts, vertices, sizeof(double) * nv * d, cudaMemcpyHostToDevice);
         if (e != cudaSuccess) { cudaFree(m->d_verts); delete m; return fail(DOGIP_E_OOM, "vertex upload failed"); }
     }
-    if (nccl_id) {   // also for nranks = 1: exercises the exchange / all-reduce plumbing
-        auto& api = nccl();
-        if (!api.ok) { dogip_mesh_destroy(m); return fail(DOGIP_E_NCCL, api.err); }
-        ncclUniqueId id;
-        std::memcpy(&id, nccl_id, sizeof id);
-        ncclResult_t r = api.CommInitRank(&m->comm, nranks, id, rank);
-        if (r != ncclSuccess) { m->comm = nullptr; dogip_mesh_destroy(m); return fail(DOGIP_E_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r)); }
+    if (comm_kind != DOGIP_COMM_NONE) {   // also for nranks = 1: exercises the exchange / all-reduce plumbing
+        int rc = 0;
+        std::string msg;
+        if (comm_kind == DOGIP_COMM_NCCL) {
+            auto* c = new NcclComm();
+            rc = c->init(comm_arg, rank, nranks);
+            msg = c->err;
+            m->comm = c;
+        } else {
+            auto* c = new LoopbackComm();
+            rc = c->init(&static_cast<dogip_loopback_s*>(const_cast<void*>(comm_arg))->g, rank, nranks);
+            msg = c->err;
+            m->comm = c;
+        }
+        if (rc) { dogip_mesh_destroy(m); return fail(rc, msg); }
         cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking);
         cudaEventCreateWithFlags(&m->ev_bnd, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&m->ev_comm, cudaEventDisableTiming);
@@ -257,7 +320,7 @@ extern "C" void dogip_mesh_destroy(dogip_mesh m) {
     if (!m) return;
     if (m->device < 0) { delete m; return; }
     DeviceGuard dg(m->device);
-    if (m->comm && nccl().ok) nccl().CommDestroy(m->comm);
+    delete m->comm;
     if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
     if (m->ev_bnd) cudaEventDestroy(m->ev_bnd);
     if (m->ev_comm) cudaEventDestroy(m->ev_comm);
@@ -309,24 +372,51 @@ static int check_coeff(int d, int form, const dogip_coeff* c, int& ncomp) {
 
 // Sum the two interface planes (P values each) of a slab vector of length n with the
 // neighbours (same plan as the apply exchange); synchronous, setup only.
+// An asynchronous communicator failure (dead peer, NCCL error) surfaces at the next call
+// on the mesh: the communicator is aborted and E_NCCL returned.
+static int comm_check(dogip_mesh_s* m) {
+    if (!m->comm) return DOGIP_OK;
+    if (const int rc = m->comm->async_error()) {
+        const std::string msg = m->comm->err;
+        m->comm->abort();
+        return fail(rc, msg);
+    }
+    return DOGIP_OK;
+}
+
+// Synchronise `st`.  With a communicator the wait polls the stream and the communicator's
+// asynchronous error state; an error, or no progress within DOGIP_COMM_TIMEOUT_S seconds
+// (default 600), aborts the communicator (ncclCommAbort releases the blocked kernels) and
+// returns E_NCCL instead of hanging on a dead peer.
+static int stream_sync(dogip_mesh_s* m, cudaStream_t st) {
+    if (!m->comm) {
+        CK(cudaStreamSynchronize(st));
+        return DOGIP_OK;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) return DOGIP_OK;
+        if (e != cudaErrorNotReady) return fail(DOGIP_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+        RET(comm_check(m));
+        const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (dt > comm_timeout_s()) {
+            m->comm->abort();
+            return fail(DOGIP_E_NCCL, "timed out waiting for the peers (DOGIP_COMM_TIMEOUT_S); communicator aborted");
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
+// Sum the two interface planes (P values each) of a slab vector of length n with the
+// neighbours (same plan as the apply exchange); synchronous, setup only.
 static int sum_interface_planes(dogip_mesh_s* m, double* v, int64_t P, int64_t n, cudaStream_t st) {
-    auto& api = nccl();
     double* rb = nullptr;
     CK(cudaMalloc(&rb, sizeof(double) * 2 * P));
     struct Free { double* p; ~Free() { cudaFree(p); } } fr{rb};
-    NK(api.GroupStart());
-    if (m->rank > 0) {
-        NK(api.Send(v, P, ncclDouble, m->rank - 1, m->comm, st));
-        NK(api.Recv(rb, P, ncclDouble, m->rank - 1, m->comm, st));
-    }
-    if (m->rank < m->nranks - 1) {
-        NK(api.Send(v + n - P, P, ncclDouble, m->rank + 1, m->comm, st));
-        NK(api.Recv(rb + P, P, ncclDouble, m->rank + 1, m->comm, st));
-    }
-    NK(api.GroupEnd());
+    CM(m, m->comm->exchange(v, v + n - P, rb, rb + P, P, st));
     CK(launch_add_planes(v, m->rank > 0 ? rb : nullptr, m->rank < m->nranks - 1 ? rb + P : nullptr, P, n - P, st));
-    CK(cudaStreamSynchronize(st));
-    return DOGIP_OK;
+    return stream_sync(m, st);
 }
 
 // Coefficient parameters as the kernels read them: the caller's array, plus for the
@@ -588,7 +678,6 @@ extern "C" void dogip_op_destroy(dogip_op op) {
     if (op->h_scal) cudaFreeHost(op->h_scal);
     if (op->cg_exec) cudaGraphExecDestroy(op->cg_exec);
     if (op->cg_graph) cudaGraphDestroy(op->cg_graph);
-    cudaFree(op->cg_it);
     if (op->cap_stream) cudaStreamDestroy(op->cap_stream);
     for (cudaEvent_t e : op->ev_in) cudaEventDestroy(e);
     for (cudaEvent_t e : op->ev_done) cudaEventDestroy(e);
@@ -600,20 +689,10 @@ extern "C" void dogip_op_destroy(dogip_op op) {
 // ------------------------------------------------------------------ apply
 static int exchange_planes(dogip_mesh_s* m, double* y, cudaEvent_t ready) {
     // sum this rank's partial interface planes with the neighbours' (A8)
-    auto& api = nccl();
     const int64_t P = m->d == 3 ? m->geo.sy * m->geo.sy : m->geo.sy;
     const int64_t last = m->geo.ndof - P;
     CK(cudaStreamWaitEvent(m->comm_stream, ready, 0));
-    NK(api.GroupStart());
-    if (m->rank > 0) {
-        NK(api.Send(y, P, ncclDouble, m->rank - 1, m->comm, m->comm_stream));
-        NK(api.Recv(m->rbuf, P, ncclDouble, m->rank - 1, m->comm, m->comm_stream));
-    }
-    if (m->rank < m->nranks - 1) {
-        NK(api.Send(y + last, P, ncclDouble, m->rank + 1, m->comm, m->comm_stream));
-        NK(api.Recv(m->rbuf + P, P, ncclDouble, m->rank + 1, m->comm, m->comm_stream));
-    }
-    NK(api.GroupEnd());
+    CM(m, m->comm->exchange(y, y + last, m->rbuf, m->rbuf + P, P, m->comm_stream));
     CK(cudaEventRecord(m->ev_comm, m->comm_stream));
     return DOGIP_OK;
 }
@@ -643,7 +722,7 @@ static QpArgs qp_args(dogip_op op, const ApplyArgs& a) {
 // y = A u (+ exchange); with dot != null also *dot = u^T y over this rank's elements
 // (+ boundary rows owned by this rank), fused into the apply kernel (CG's p.q).
 static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, cudaStream_t st,
-                      double* dot = nullptr) {
+                      double* dot = nullptr, const double* skip_if = nullptr) {
     dogip_mesh_s* m = op->m;
     const SlabGeo& g = m->geo;
     CK(cudaMemsetAsync(y, 0, sizeof(double) * g.ndof, st));
@@ -654,6 +733,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
     a.u = u; a.y = y; a.w = op->d_w; a.geo = g; a.tab = &m->tab;
     a.num_sms = m->num_sms;
     a.stream = st;
+    a.skip_if = skip_if;
     int nslots[3] = {0, 0, 0};
     int nl = 0;
     if (dot && !op->dotp) {
@@ -712,6 +792,7 @@ extern "C" int dogip_apply(dogip_op op, const double* u, double* y, unsigned fla
     RET(check_vec(y, "y"));
     if (u == y) return fail(DOGIP_E_INVALID_ARG, "u and y must not alias");
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
+    RET(comm_check(op->m));
     return apply_impl(op, u, y, flags, (cudaStream_t)stream);
 }
 
@@ -796,13 +877,14 @@ extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_hos
     CK(cudaMemcpyAsync(op->hu, u_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     RET(dogip_apply(op, op->hu, op->hy, flags, stream));
     CK(cudaMemcpyAsync(y_host, op->hy, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    RET(stream_sync(op->m, st));
     return DOGIP_OK;
 }
 
 extern "C" int dogip_load_vector(dogip_op op, double f, double* b, unsigned flags, void* stream) {
     if (!op) return fail(DOGIP_E_INVALID_ARG, "null argument");
     RET(check_vec(b, "b"));
+    RET(comm_check(op->m));
     cudaStream_t st = (cudaStream_t)stream;
     dogip_mesh_s* m = op->m;
     CK(cudaMemsetAsync(b, 0, sizeof(double) * m->geo.ndof, st));
@@ -818,27 +900,41 @@ extern "C" int dogip_load_vector(dogip_op op, double f, double* b, unsigned flag
 
 // ------------------------------------------------------------------ CG
 static int allreduce_scalar(dogip_mesh_s* m, double* s, cudaStream_t st) {
-    if (m->comm) NK(nccl().AllReduce(s, s, 1, ncclDouble, ncclSum, m->comm, st));
+    if (m->comm) CM(m, m->comm->allreduce_sum(s, 1, st));
     return DOGIP_OK;
 }
 
 extern "C" int64_t dogip_kernel_launches(void) { return (int64_t)g_launches.load(); }
 
-// The CG iterations of a solve as one CUDA graph: a conditional WHILE node whose body is
-// one iteration (apply with fused p.q, r update + r.r, x/p update, cg_control), so the
-// loop runs without a host round trip per iteration; cg_control sets the condition.
-// Single rank only (the multi-rank loop all-reduces through NCCL between kernels).
-// Rebuilt when x, the flags, rtol, maxit or the stream change.
-static int cg_graph_build(dogip_op op, double* x, double rtol, int maxit, unsigned aflags, cudaStream_t st) {
+// One CG iteration (Hestenes-Stiefel, reading L15), every step on the device:
+//   q = A p, p.q fused into the apply            [all-reduce p.q]
+//   r -= alpha q, r.r                            [all-reduce r.r]
+//   x += alpha p, p = r + beta p
+//   control: breakdown / count / convergence / maxit -> S_DONE (graph path: WHILE condition)
+// An iteration enqueued after the solve finished is a no-op (the apply kernel returns at
+// once and alpha = 0), so batches of iterations are enqueued without a host round trip.
+static int cg_iteration(dogip_op op, double* x, unsigned aflags, double rtol, int maxit,
+                        const cudaGraphConditionalHandle* h, cudaStream_t st, cudaEvent_t ev0 = nullptr,
+                        cudaEvent_t ev1 = nullptr) {
     dogip_mesh_s* m = op->m;
-    const int64_t n = m->geo.ndof;
     dogip_mesh_info_t info;
     dogip_mesh_info(m, &info);
-    if (!op->cg_it) CK(cudaMalloc(&op->cg_it, sizeof(int)));
-    if (!op->dotp) {
-        CK(cudaMalloc(&op->dotp, sizeof(double) * 3 * APPLY_MAX_WARPS));
-        CK(cudaMalloc(&op->bpart, sizeof(double) * RED_BLOCKS));
-    }
+    const int64_t n = m->geo.ndof;
+    if (ev0) CK(cudaEventRecord(ev0, st));
+    RET(apply_impl(op, op->pv, op->q, aflags, st, op->scal + S_PQ, op->scal + S_DONE));   // q = A p
+    if (ev1) CK(cudaEventRecord(ev1, st));
+    RET(allreduce_scalar(m, op->scal + S_PQ, st));
+    CK(launch_cg_r(op->r, op->q, n, info.owned_begin, info.owned_end, op->scal, op->partials, st));
+    RET(allreduce_scalar(m, op->scal + S_RRNEW, st));
+    CK(launch_cg_px(x, op->pv, op->r, n, op->scal, st));
+    CK(launch_cg_control(op->scal, rtol, maxit, h, st));
+    return DOGIP_OK;
+}
+
+// The CG iterations of a single-rank solve as one CUDA graph: a conditional WHILE node
+// whose body is one cg_iteration; its control kernel sets the condition, so the loop runs
+// without a host round trip.  Rebuilt when x, the flags, rtol, maxit or the stream change.
+static int cg_graph_build(dogip_op op, double* x, double rtol, int maxit, unsigned aflags, cudaStream_t st) {
     auto& k = op->cg_key;
     if (!op->cg_exec || k.x != x || k.flags != aflags || k.rtol != rtol || k.maxit != maxit || k.st != st) {
         if (op->cg_exec) { cudaGraphExecDestroy(op->cg_exec); op->cg_exec = nullptr; }
@@ -857,30 +953,14 @@ static int cg_graph_build(dogip_op op, double* x, double rtol, int maxit, unsign
         if (!op->cap_stream) CK(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
         cudaStream_t cs = op->cap_stream;
         CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        int rc = apply_impl(op, op->pv, op->q, aflags, cs, op->scal + S_PQ);     // q = A p, p.q fused
-        cudaError_t ce = cudaSuccess;
-        if (rc >= 0) ce = launch_cg_r(op->r, op->q, n, info.owned_begin, info.owned_end, op->scal, op->partials, cs);
-        if (rc >= 0 && ce == cudaSuccess) ce = launch_cg_px(x, op->pv, op->r, n, op->scal, cs);
-        if (rc >= 0 && ce == cudaSuccess) ce = launch_cg_control(op->scal, op->cg_it, rtol, maxit, h, cs);
+        const int rc = cg_iteration(op, x, aflags, rtol, maxit, &h, cs);
         cudaGraph_t captured = nullptr;
         const cudaError_t ee = cudaStreamEndCapture(cs, &captured);
         if (rc < 0) return rc;
-        CK(ce);
         CK(ee);
         CK(cudaGraphInstantiate(&op->cg_exec, op->cg_graph, 0));
         k.x = x; k.flags = aflags; k.rtol = rtol; k.maxit = maxit; k.st = st;
     }
-    return DOGIP_OK;
-}
-
-static int cg_graph_run(dogip_op op, cudaStream_t st, int* iters) {
-    CK(cudaMemsetAsync(op->cg_it, 0, sizeof(int), st));
-    CK(cudaGraphLaunch(op->cg_exec, st));
-    CK(cudaMemcpyAsync(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
-    int it = 0;
-    CK(cudaMemcpyAsync(&it, op->cg_it, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    *iters = it;
     return DOGIP_OK;
 }
 
@@ -892,6 +972,7 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_CG_RESUME)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
     cudaStream_t st = (cudaStream_t)stream;
     dogip_mesh_s* m = op->m;
+    RET(comm_check(m));
     const int64_t n = m->geo.ndof;
     dogip_mesh_info_t info;
     dogip_mesh_info(m, &info);
@@ -906,26 +987,30 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
         CK(cudaMalloc(&op->scal, sizeof(double) * S_COUNT));
         CK(cudaMallocHost(&op->h_scal, sizeof(double) * S_COUNT));
     }
+    if (!op->dotp) {
+        CK(cudaMalloc(&op->dotp, sizeof(double) * 3 * APPLY_MAX_WARPS));
+        CK(cudaMalloc(&op->bpart, sizeof(double) * RED_BLOCKS));
+    }
     const unsigned aflags = flags & DOGIP_DIRICHLET_ZERO;
     const bool bench = maxit < 0;
     const int nit = bench ? -maxit : maxit;
-    cudaEvent_t t0, t1, ready;
+    const double rtol_dev = bench ? -1.0 : rtol;      // fixed-count runs never test convergence
+    cudaEvent_t t0, t1;
     CK(cudaEventCreate(&t0));
     CK(cudaEventCreate(&t1));
-    CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
     std::vector<cudaEvent_t> aev;
     struct EvGuard {
-        cudaEvent_t a, b, c;
+        cudaEvent_t a, b;
         std::vector<cudaEvent_t>* v;
-        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c); for (auto e : *v) cudaEventDestroy(e); }
-    } guard{t0, t1, ready, &aev};
+        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); for (auto e : *v) cudaEventDestroy(e); }
+    } guard{t0, t1, &aev};
     if (bench) {
         aev.resize(2 * (size_t)nit);
         for (auto& e : aev) CK(cudaEventCreate(&e));
     }
-    // the graph-captured loop is built (or reused) before the timed region
-    const bool graph_ok = !bench && nit > 0 && !m->comm && std::getenv("DOGIP_CG_NO_GRAPH") == nullptr;
-    if (graph_ok) RET(cg_graph_build(op, x, rtol, nit, aflags, st));
+    // single rank: the graph-captured loop is built (or reused) before the timed region
+    const bool graph = !bench && nit > 0 && !m->comm && std::getenv("DOGIP_CG_NO_GRAPH") == nullptr;
+    if (graph) RET(cg_graph_build(op, x, rtol_dev, nit, aflags, st));
     CK(cudaEventRecord(t0, st));
     if (!resume) {
         // r = b - A x ; p = r
@@ -938,64 +1023,53 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
     }
     CK(launch_dot(b, b, o0, o1, op->partials, op->scal + S_BB, st));
     RET(allreduce_scalar(m, op->scal + S_BB, st));
-    double rr = 0.0, bnorm = 0.0;
+    CK(launch_cg_init(op->scal, rtol_dev, st));
     if (!bench) {
+        // one host read per solve: b = 0 returns x untouched; ||r_0|| small enough stops here
         CK(cudaMemcpyAsync(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        bnorm = std::sqrt(op->h_scal[S_BB]);
-        rr = op->h_scal[S_RR];
-        if (bnorm == 0.0) {
+        RET(stream_sync(m, st));
+        if (op->h_scal[S_BB] == 0.0) {
             res->iters = 0; res->status = DOGIP_OK; res->rel_res = 0.0; res->seconds = 0.0; res->apply_seconds = 0.0;
             return DOGIP_OK;
         }
-    }
-    int it = 0, status = DOGIP_OK;
-    const bool graph = graph_ok && !(std::sqrt(rr) <= rtol * bnorm);
-    if (graph) {
-        RET(cg_graph_run(op, st, &it));
-        rr = op->h_scal[S_RR];
-        if (!(op->h_scal[S_PQ] > 0.0)) status = DOGIP_E_BREAKDOWN;
-        else if (!(std::sqrt(rr) <= rtol * bnorm)) status = DOGIP_NOT_CONVERGED;
-    }
-    while (!graph) {
-        if (!bench && std::sqrt(rr) <= rtol * bnorm) break;
-        if (it >= nit) { status = bench ? DOGIP_OK : DOGIP_NOT_CONVERGED; break; }
-        if (bench) CK(cudaEventRecord(aev[2 * it], st));
-        RET(apply_impl(op, op->pv, op->q, aflags, st, op->scal + S_PQ));      // q = A p, p.q fused
-        if (bench) CK(cudaEventRecord(aev[2 * it + 1], st));
-        RET(allreduce_scalar(m, op->scal + S_PQ, st));
-        CK(launch_cg_r(op->r, op->q, n, o0, o1, op->scal, op->partials, st));  // r -= alpha q, r.r
-        RET(allreduce_scalar(m, op->scal + S_RRNEW, st));
-        if (!bench) {
-            CK(cudaMemcpyAsync(op->h_scal + S_PQ, op->scal + S_PQ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
-            CK(cudaEventRecord(ready, st));
+        if (op->h_scal[S_DONE] == 0.0 && nit > 0) {
+            if (graph) {
+                CK(cudaGraphLaunch(op->cg_exec, st));
+            } else {
+                // eagerly enqueued batches of predicated iterations, one host read per batch
+                int batch = 32;
+                if (const char* e = std::getenv("DOGIP_CG_BATCH")) batch = std::max(1, std::atoi(e));
+                for (int enq = 0; enq < nit;) {
+                    const int kk = std::min(batch, nit - enq);
+                    for (int i = 0; i < kk; ++i) RET(cg_iteration(op, x, aflags, rtol_dev, nit, nullptr, st));
+                    enq += kk;
+                    CK(cudaMemcpyAsync(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
+                    RET(stream_sync(m, st));
+                    if (op->h_scal[S_DONE] != 0.0) break;
+                }
+            }
         }
-        CK(launch_cg_px(x, op->pv, op->r, n, op->scal, st));                  // x += alpha p, p = r + beta p
-        ++it;
-        if (!bench) {
-            CK(cudaEventSynchronize(ready));
-            if (!(op->h_scal[S_PQ] > 0.0)) { status = DOGIP_E_BREAKDOWN; rr = op->h_scal[S_RRNEW]; break; }
-            rr = op->h_scal[S_RRNEW];
-        }
+    } else {
+        for (int i = 0; i < nit; ++i) RET(cg_iteration(op, x, aflags, rtol_dev, nit, nullptr, st, aev[2 * i], aev[2 * i + 1]));
     }
     CK(cudaEventRecord(t1, st));
-    CK(cudaStreamSynchronize(st));
-    if (bench) {
-        CK(cudaMemcpy(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost));
-        rr = op->h_scal[S_RR];
-        bnorm = std::sqrt(op->h_scal[S_BB]);
-    }
+    CK(cudaMemcpyAsync(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
+    RET(stream_sync(m, st));
+    const double* hs = op->h_scal;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, t0, t1);
     double aps = 0.0;
-    for (int i = 0; i < (bench ? it : 0); ++i) {
+    for (int i = 0; i < (bench ? nit : 0); ++i) {
         float a = 0.f;
         cudaEventElapsedTime(&a, aev[2 * i], aev[2 * i + 1]);
         aps += a * 1e-3;
     }
-    res->iters = it;
+    int status = (int)hs[S_STATUS];
+    if (hs[S_DONE] == 0.0) status = DOGIP_NOT_CONVERGED;        // maxit = 0, or batches exhausted
+    if (bench && status == DOGIP_NOT_CONVERGED) status = DOGIP_OK;
+    res->iters = (int)hs[S_IT];
     res->status = status;
-    res->rel_res = bnorm > 0 ? std::sqrt(rr) / bnorm : 0.0;
+    res->rel_res = hs[S_BB] > 0 ? std::sqrt(hs[S_RR]) / std::sqrt(hs[S_BB]) : 0.0;
     res->seconds = ms * 1e-3;
     res->apply_seconds = aps;
     if (status == DOGIP_E_BREAKDOWN) return fail(DOGIP_E_BREAKDOWN, "CG breakdown: p^T A p <= 0");
@@ -1167,6 +1241,29 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
                     host[(e * WT + j) * NC + c] =
                         op->store == DOGIP_STORE_ISO ? at(op->ref.NG + op->ref.rowperm[j]) * at(c) : at(j * NC + c);
         }
+    return DOGIP_OK;
+}
+
+extern "C" int dogip_test_perturb_weight(dogip_op op, int64_t elem, int j, int c, double delta) {
+    if (!op) return fail(DOGIP_E_INVALID_ARG, "null argument");
+    if (op->store != DOGIP_STORE_FULL) return fail(DOGIP_E_INVALID_ARG, "perturbation hook: DOGIP_STORE_FULL only");
+    const SlabGeo& g = op->m->geo;
+    dogip_mesh_info_t info;
+    dogip_mesh_info(op->m, &info);
+    const int NC = op->ref.NC;
+    if (elem < 0 || elem >= info.n_elem_local || j < 0 || j >= op->ref.WT || c < 0 || c >= NC)
+        return fail(DOGIP_E_INVALID_SIZE, "perturbation hook: index out of range");
+    // canonical e = ns * cell + s, cell = ci + Nx (cj + Ny ck) -> tile (s fastest, then x-block,
+    // row, layer) and lane ci % 32, the inverse of canonical_elem
+    const int64_t s = elem % g.ns, cell = elem / g.ns;
+    const int64_t ci = cell % g.Nx, cj = (cell / g.Nx) % g.Ny, ck = cell / ((int64_t)g.Nx * g.Ny);
+    const int64_t tile = s + g.ns * (ci / TILE + g.nxb * (cj + (int64_t)g.Ny * ck));
+    const size_t idx = ((size_t)tile * op->ref.tile_rows + (size_t)(j * NC + c)) * TILE + (size_t)(ci % TILE);
+    DeviceGuard dg(op->m->device);
+    double v = 0.0;
+    CK(cudaMemcpy(&v, op->d_w + idx, sizeof(double), cudaMemcpyDeviceToHost));
+    v += delta;
+    CK(cudaMemcpy(op->d_w + idx, &v, sizeof(double), cudaMemcpyHostToDevice));
     return DOGIP_OK;
 }
 

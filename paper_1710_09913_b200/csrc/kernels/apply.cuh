@@ -76,6 +76,8 @@ struct ApplyArgs {
     double* dot_partials;      // != null: per-warp partials of u^T A u (APPLY_MAX_WARPS slots)
     int* dot_nslots;           // out: number of partial slots written
     const int* offw;           // global WP: device table [NS][W_T] of W-lattice offsets
+    const double* skip_if;     // != null: the kernel returns at once when *skip_if != 0 (an
+                               // iteration enqueued after its CG solve finished)
 };
 
 cudaError_t launch_apply(const ApplyArgs& a);
@@ -187,9 +189,16 @@ cudaError_t launch_cg_r(double* r, const double* q, int64_t n, int64_t i0, int64
 // x += alpha p; p = r + beta p (beta = scal[RRNEW]/scal[RR]); then scal[RR] = scal[RRNEW]
 cudaError_t launch_cg_px(double* x, double* p, const double* r, int64_t n, double* scal, cudaStream_t st);
 
-enum CgScal { S_RR = 0, S_PQ = 1, S_RRNEW = 2, S_BB = 3, S_COUNT = 8 };
-// graph-captured CG: ++*it_d; conditional = !(converged || breakdown || *it_d >= maxit)
-cudaError_t launch_cg_control(const double* scal, int* it_d, double rtol, int maxit, cudaGraphConditionalHandle h,
+// device scalars of a CG solve: S_DONE / S_IT / S_STATUS are the loop state (cg_control)
+enum CgScal { S_RR = 0, S_PQ = 1, S_RRNEW = 2, S_BB = 3, S_DONE = 4, S_IT = 5, S_STATUS = 6, S_COUNT = 8 };
+// after an iteration: breakdown / count / convergence / maxit -> S_DONE, S_STATUS; with h
+// (graph path) also the WHILE node's condition = !S_DONE
+cudaError_t launch_cg_control(double* scal, double rtol, int maxit, const cudaGraphConditionalHandle* h,
                               cudaStream_t st);
+// S_IT = 0, S_DONE = (||r_0|| <= rtol ||b||), rtol < 0: never converged (fixed-count runs)
+cudaError_t launch_cg_init(double* scal, double rtol, cudaStream_t st);
+// loopback all-reduce: out[i] = sum_k slots[k stride + i], k = 0..nranks-1 in order
+cudaError_t launch_sum_slots(const double* slots, int nranks, int64_t stride, int64_t n, double* out,
+                             cudaStream_t st);
 
 }  // namespace dogip

@@ -306,7 +306,9 @@ template <int D, int P, int F, int ST, bool DIR, bool GLOB>
 __global__ void __launch_bounds__(APPLY_THREADS, min_blocks<dogip_gen::RefElem<D, P, F, ST>>())
 apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
              const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end,
-             double* __restrict__ dot_partials, const int* __restrict__ offw_g) {
+             double* __restrict__ dot_partials, const int* __restrict__ offw_g,
+             const double* __restrict__ skip_if) {
+    if (skip_if && *skip_if != 0.0) return;    // finished CG solve: the weight stream is not read
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
@@ -471,7 +473,7 @@ cudaError_t launch_one(const ApplyArgs& a) {
         return cudaSuccess;
     }
     kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, a.tile_begin,
-                                                           a.tile_end, a.dot_partials, a.offw);
+                                                           a.tile_end, a.dot_partials, a.offw, a.skip_if);
     count_launches(1);
     return cudaGetLastError();
 }

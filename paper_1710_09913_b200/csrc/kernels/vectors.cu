@@ -66,11 +66,22 @@ __global__ void __launch_bounds__(RED_THREADS) reduce_final_kernel(const double*
     if (threadIdx.x == 0) *out = s;
 }
 
+// CG step sizes from the device scalars.  The iteration is a no-op once the solve is done
+// (S_DONE, set by cg_control: converged, breakdown or maxit -- the eagerly enqueued batches
+// of the multi-rank loop run past that point) and on breakdown (p.q <= 0: x is left at the
+// last iterate, as the oracle's CG returns it).
+__device__ __forceinline__ double cg_alpha(const double* scal) {
+    return (scal[S_DONE] != 0.0 || !(scal[S_PQ] > 0.0)) ? 0.0 : scal[S_RR] / scal[S_PQ];
+}
+__device__ __forceinline__ double cg_beta(const double* scal) {
+    return scal[S_RR] > 0.0 ? scal[S_RRNEW] / scal[S_RR] : 0.0;
+}
+
 __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__ x, double* __restrict__ r,
                                                             const double* __restrict__ p,
                                                             const double* __restrict__ q, int64_t n, int64_t i0,
                                                             int64_t i1, const double* scal, double* partials) {
-    const double alpha = scal[S_RR] / scal[S_PQ];
+    const double alpha = cg_alpha(scal);
     double2* x2 = reinterpret_cast<double2*>(x);
     double2* r2 = reinterpret_cast<double2*>(r);
     const double2* p2 = reinterpret_cast<const double2*>(p);
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(RED_THREADS) cg_xr_kernel(double* __restrict__
 
 __global__ void __launch_bounds__(RED_THREADS) cg_p_kernel(double* __restrict__ p, const double* __restrict__ r,
                                                            int64_t n, const double* scal) {
-    const double beta = scal[S_RRNEW] / scal[S_RR];
+    const double beta = cg_beta(scal);
     double2* p2 = reinterpret_cast<double2*>(p);
     const double2* r2 = reinterpret_cast<const double2*>(r);
     const int64_t np = n / 2;
@@ -141,15 +152,46 @@ __global__ void __launch_bounds__(RED_THREADS) cg_p_kernel(double* __restrict__ 
 
 __global__ void shift_rr_kernel(double* scal) { scal[S_RR] = scal[S_RRNEW]; }
 
-// device-side loop control of the graph-captured CG (conditional WHILE node): count the
-// iteration, stop on convergence ||r|| <= rtol ||b||, breakdown p.q <= 0 or maxit
-__global__ void cg_control_kernel(const double* scal, int* it_d, double rtol, int maxit,
-                                  cudaGraphConditionalHandle h) {
-    const int it = *it_d + 1;
-    *it_d = it;
-    const bool breakdown = !(scal[S_PQ] > 0.0);
-    const bool conv = sqrt(scal[S_RR]) <= rtol * sqrt(scal[S_BB]);
-    cudaGraphSetConditional(h, (!breakdown && !conv && it < maxit) ? 1u : 0u);
+// Device-side loop control after each CG iteration: a breakdown (p.q <= 0, the iteration
+// made no update) ends the solve without counting it; otherwise count the iteration and
+// stop on ||r|| <= rtol ||b|| or maxit.  Graph path: also sets the WHILE node's condition.
+__global__ void cg_control_kernel(double* scal, double rtol, int maxit, cudaGraphConditionalHandle h, int use_h) {
+    if (scal[S_DONE] == 0.0) {
+        if (!(scal[S_PQ] > 0.0)) {
+            scal[S_DONE] = 1.0;
+            scal[S_STATUS] = -9.0;                 // DOGIP_E_BREAKDOWN
+        } else {
+            const double it = scal[S_IT] + 1.0;
+            scal[S_IT] = it;
+            if (sqrt(scal[S_RR]) <= rtol * sqrt(scal[S_BB])) {
+                scal[S_DONE] = 1.0;
+                scal[S_STATUS] = 0.0;              // DOGIP_OK
+            } else if (it >= (double)maxit) {
+                scal[S_DONE] = 1.0;
+                scal[S_STATUS] = 1.0;              // DOGIP_NOT_CONVERGED
+            }
+        }
+    }
+    if (use_h) cudaGraphSetConditional(h, scal[S_DONE] == 0.0 ? 1u : 0u);
+}
+
+// start of a solve: counters reset; done at once if ||r_0|| <= rtol ||b|| (rtol < 0: never)
+__global__ void cg_init_kernel(double* scal, double rtol) {
+    scal[S_IT] = 0.0;
+    scal[S_STATUS] = 1.0;
+    const bool conv = rtol >= 0.0 && sqrt(scal[S_RR]) <= rtol * sqrt(scal[S_BB]);
+    scal[S_DONE] = conv ? 1.0 : 0.0;
+    if (conv) scal[S_STATUS] = 0.0;
+}
+
+// in-process all-reduce of the loopback communicator: out[i] = sum_k slots[k stride + i],
+// ranks in fixed order (identical bits on every rank)
+__global__ void sum_slots_kernel(const double* slots, int nranks, int64_t stride, int64_t n, double* out) {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < nranks; ++k) s += slots[k * stride + i];
+        out[i] = s;
+    }
 }
 
 __global__ void axpby_kernel(double* y, const double* x, double a, double b, int64_t n) {
@@ -250,7 +292,7 @@ __global__ void __launch_bounds__(RED_THREADS) sum_partials_kernel(const double*
 __global__ void __launch_bounds__(RED_THREADS) cg_r_kernel(double* __restrict__ r, const double* __restrict__ q,
                                                            int64_t n, int64_t i0, int64_t i1, const double* scal,
                                                            double* partials) {
-    const double alpha = scal[S_RR] / scal[S_PQ];
+    const double alpha = cg_alpha(scal);
     double2* r2 = reinterpret_cast<double2*>(r);
     const double2* q2 = reinterpret_cast<const double2*>(q);
     const int64_t np = n / 2;
@@ -289,8 +331,8 @@ __global__ void __launch_bounds__(RED_THREADS) cg_r_kernel(double* __restrict__ 
 __global__ void __launch_bounds__(RED_THREADS) cg_px_kernel(double* __restrict__ x, double* __restrict__ p,
                                                             const double* __restrict__ r, int64_t n,
                                                             const double* scal) {
-    const double alpha = scal[S_RR] / scal[S_PQ];
-    const double beta = scal[S_RRNEW] / scal[S_RR];
+    const double alpha = cg_alpha(scal);
+    const double beta = cg_beta(scal);
     double2* x2 = reinterpret_cast<double2*>(x);
     double2* p2 = reinterpret_cast<double2*>(p);
     const double2* r2 = reinterpret_cast<const double2*>(r);
@@ -354,9 +396,22 @@ cudaError_t launch_cg_p(double* p, const double* r, int64_t n, double* scal, cud
     return cudaGetLastError();
 }
 
-cudaError_t launch_cg_control(const double* scal, int* it_d, double rtol, int maxit, cudaGraphConditionalHandle h,
+cudaError_t launch_cg_control(double* scal, double rtol, int maxit, const cudaGraphConditionalHandle* h,
                               cudaStream_t st) {
-    cg_control_kernel<<<1, 1, 0, st>>>(scal, it_d, rtol, maxit, h);
+    cg_control_kernel<<<1, 1, 0, st>>>(scal, rtol, maxit, h ? *h : cudaGraphConditionalHandle{}, h != nullptr);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_init(double* scal, double rtol, cudaStream_t st) {
+    cg_init_kernel<<<1, 1, 0, st>>>(scal, rtol);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum_slots(const double* slots, int nranks, int64_t stride, int64_t n, double* out,
+                             cudaStream_t st) {
+    sum_slots_kernel<<<1, 64, 0, st>>>(slots, nranks, stride, n, out);
     count_launches(1);
     return cudaGetLastError();
 }

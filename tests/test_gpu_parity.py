@@ -241,7 +241,7 @@ def test_slab_partials_sum_to_global(d, N, p, form, nr):
 
 
 HOST_CASES = [("C4", 9, 1, 0, False), ("C4", 9, 1, 0, True), ("C4", 37, 1, 0, True), ("C2p2", 40, 1, 0, True),
-              ("C5", 5, 0, 0, False), ("C5", 19, 0, 3, False), ("C5", 6, 0, 2, False), ("C1", 16, 0, 0, False),
+              ("C5", 5, 0, 0, False), ("C5", 19, 0, 5, False), ("C5", 6, 0, 2, False), ("C1", 16, 0, 0, False),
               ("C3", 1, 1, 0, True)]
 
 

@@ -274,3 +274,18 @@ def test_wp_total_is_one_A_one(d, p):
     assert oa.wp_total(ed, coef, chunk=5, workers=2) == pytest.approx(t, rel=1e-15)
     # closed form: m = 1 gives |Omega| = 1 on any (jittered) mesh
     assert abs(oa.wp_total(ed, Coefficient(COEF_CONST, np.array([1.0]))) - 1.0) <= 1e-14
+
+
+def test_qp_route_threads_equal_sequential_on_large_chunks():
+    """Threaded chunks (the full-size residual checks use workers > 1) give the sequential
+    result on chunks big enough for a multithreaded BLAS GEMM -- the configuration in which
+    concurrent OpenBLAS calls once corrupted the full-size C3 check."""
+    from synth.configs import get_config
+    c = get_config("C3").with_size(16)
+    ed = oa.build(3, 16, 2)
+    coef = c.coefficient()
+    u = c.u()
+    y1 = oa.apply_qp_route(ed, 1, coef, u, workers=1, chunk=8192)
+    for _ in range(3):
+        y8 = oa.apply_qp_route(ed, 1, coef, u, workers=8, chunk=8192)
+        assert np.abs(y8 - y1).max() <= 1e-15 * np.abs(y1).max()
