@@ -734,6 +734,8 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
     a.num_sms = m->num_sms;
     a.stream = st;
     a.skip_if = skip_if;
+    bool rows_written = false;
+    a.rows_written = &rows_written;
     int nslots[3] = {0, 0, 0};
     int nl = 0;
     if (dot && !op->dotp) {
@@ -773,7 +775,9 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
         for (int i = 0; i < nl; ++i)
             CK(launch_sum_partials(op->dotp + (size_t)i * APPLY_MAX_WARPS, nslots[i], i ? dot : nullptr, dot, st));
     }
-    if (a.dirichlet) {
+    // the cell-per-lane kernel (p <= 2) writes the Dirichlet rows itself (one owner per row,
+    // its u_i^2 in the fused dot); the other kernels take the separate fix-up
+    if (a.dirichlet && !rows_written) {
         if (dot) {
             dogip_mesh_info_t info;
             dogip_mesh_info(m, &info);
@@ -801,8 +805,9 @@ extern "C" int dogip_apply(dogip_op op, const double* u, double* y, unsigned fla
 // and the copy-out of the y planes chunk c completed run on three streams.  Tiles are
 // ordered with the slab axis slowest, so chunk c = layers [a, b) = tiles [a tpl, b tpl)
 // reads DoF planes [p a, p b] and completes planes [p a, p b) (the last chunk also p b).
-// Dirichlet rows (y_i = u_i) are written per completed plane range; the DIRICHLET apply
-// kernel never scatters into boundary DoFs, so the order against later chunks is free.
+// Dirichlet rows (y_i = u_i) are written per completed plane range (the cell kernel writes
+// them itself, in the chunk holding the row's floor cell); the DIRICHLET kernels never
+// scatter into boundary DoFs, so the order against later chunks is free.
 static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_host, unsigned flags,
                                 cudaStream_t st) {
     dogip_mesh_s* m = op->m;
@@ -848,9 +853,12 @@ static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_hos
         aa.stream = st;
         aa.tile_begin = a * tpl;
         aa.tile_end = b * tpl;
+        bool rows_written = false;
+        aa.rows_written = &rows_written;
         CK(op->store == DOGIP_STORE_QP ? launch_qp_apply(qp_args(op, aa)) : launch_apply(aa));
         const int64_t done = c == K - 1 ? p * b + 1 : p * b;    // planes [out_end, done) are final
-        if (dir) CK(launch_dirichlet_planes(g, op->hu, op->hy, out_end, done, st));
+        // Dirichlet rows: written by the cell kernel of the chunk owning them, else here
+        if (dir && !rows_written) CK(launch_dirichlet_planes(g, op->hu, op->hy, out_end, done, st));
         CK(cudaEventRecord(op->ev_done[c], st));
         CK(cudaStreamWaitEvent(op->s_d2h, op->ev_done[c], 0));
         CK(cudaMemcpyAsync(y_host + out_end * plane, op->hy + out_end * plane,

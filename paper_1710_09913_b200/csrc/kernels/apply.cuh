@@ -78,6 +78,8 @@ struct ApplyArgs {
     const int* offw;           // global WP: device table [NS][W_T] of W-lattice offsets
     const double* skip_if;     // != null: the kernel returns at once when *skip_if != 0 (an
                                // iteration enqueued after its CG solve finished)
+    bool* rows_written;        // out (optional): set when the launched kernel wrote the Dirichlet
+                               // rows y_i = u_i itself (cell kernel), so no fix-up is needed
 };
 
 cudaError_t launch_apply(const ApplyArgs& a);

@@ -666,8 +666,8 @@ __device__ __forceinline__ void cell_gather(const double* __restrict__ u, const 
 }
 
 template <int D, int P, bool DIR>
-__device__ __forceinline__ void cell_scatter(double* __restrict__ y, const SlabGeo& g, const CellCtx& c,
-                                             int lane, double* yc) {
+__device__ __forceinline__ void cell_scatter(double* __restrict__ y, const double* __restrict__ u, const SlabGeo& g,
+                                             const CellCtx& c, int lane, double* yc, double* udot) {
     constexpr int Q = P + 1, NZ = D == 3 ? Q : 1;
     // the left lane's x = p face joins this lane's x = 0 face
 #pragma unroll
@@ -685,8 +685,21 @@ __device__ __forceinline__ void cell_scatter(double* __restrict__ y, const SlabG
         for (int yy = 0; yy < Q; ++yy)
 #pragma unroll
             for (int x = 0; x < Q; ++x) {
+                if (DIR && cell_bnd<D, P>(g, c, x, yy, z)) {
+                    // Dirichlet row y_i = u_i, written once: by the DoF's floor cell (offset < p
+                    // on every axis, or the cell on the upper domain face / upper slab end)
+                    const bool own = (x < P || c.ci == g.Nx - 1) &&
+                                     (yy < P || (c.cj == g.Ny - 1 && (D == 3 || g.bnd_hi))) &&
+                                     (D == 2 || z < P || (c.ck == g.Nz - 1 && g.bnd_hi));
+                    if (own) {
+                        const int64_t i = c.base + x + g.sy * yy + g.sz * z;
+                        const double v = ldg_f64(u + i);
+                        y[i] = v;
+                        if (udot) *udot = fma(v, v, *udot);
+                    }
+                    continue;
+                }
                 if (x == P && !c.last) continue;
-                if (DIR && cell_bnd<D, P>(g, c, x, yy, z)) continue;
                 red_add_f64(y + c.base + x + g.sy * yy + g.sz * z, yc[x + Q * (yy + Q * z)]);
             }
 }
@@ -767,7 +780,7 @@ apply_cell_kernel(const double* __restrict__ u, double* __restrict__ y, const do
             cell_gather<D, P, DIR>(u, geo, cur, lane, uc);
             loadw(ct + nw);
         }
-        cell_scatter<D, P, DIR>(y, geo, prev, lane, yc);
+        cell_scatter<D, P, DIR>(y, u, geo, prev, lane, yc, dot_partials ? &udot : nullptr);
     }
     if constexpr (!DW) lockstep_tail<CR, C>(gw, ct_end, ct_begin + (int64_t)blockIdx.x * NW, nw);
     if (dot_partials) {
@@ -801,6 +814,7 @@ cudaError_t launch_cell(const ApplyArgs& a) {
         return cudaSuccess;
     }
     kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, c0, c1, a.dot_partials, a.skip_if);
+    if (DIR && a.rows_written) *a.rows_written = true;   // Dirichlet rows written in-kernel
     count_launches(1);
     return cudaGetLastError();
 }
