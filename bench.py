@@ -314,6 +314,42 @@ def alg_bytes(oinfo: dict, n_elem: int, ndof: int) -> int:
     return 8 * n_w * n_elem + 16 * ndof
 
 
+def graph_timed_apply(torch, op, u, y, dirichlet, flush, K):
+    """Device time of one apply (memset of y + kernel(s) + fix-up, i.e. dogip_apply),
+    with the L2 flushed before each: K x (flush, apply) and K x (flush) are each captured
+    in a CUDA graph and replayed, so no host launch gap is timed (a 10-20 us Python call
+    would dominate the small configs); apply = (t_both - t_flush) / K.  Returns (median
+    per-apply seconds over 5 replays, list)."""
+    g_both, g_flush = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for k in range(2):                                   # warm the capture stream
+            flush.fill_(1.0)
+            op.apply(u, y, dirichlet=dirichlet)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g_both):
+        for k in range(K):
+            flush.fill_(float(k))
+            op.apply(u, y, dirichlet=dirichlet)
+    with torch.cuda.graph(g_flush):
+        for k in range(K):
+            flush.fill_(float(k))
+    out = []
+    for _ in range(5):
+        tt = []
+        for g in (g_both, g_flush):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            e1.synchronize()
+            tt.append(e0.elapsed_time(e1) * 1e-3)
+        out.append((tt[0] - tt[1]) / K)
+    return float(np.median(out)), out
+
+
 def secondary_configs(args, stream) -> list:
     """Every BASELINE.json config on this GPU, each apply timed alone with the L2 flushed
     before it (a 256 MB write; median of K), plus CG ms per iteration (fixed count, warm)."""
@@ -336,30 +372,43 @@ def secondary_configs(args, stream) -> list:
         y = torch.empty_like(u)
         for _ in range(3):
             op.apply(u, y, dirichlet=dirichlet)
-        ts = []
-        for k in range(K):
+        sampler = ClockSampler(torch.cuda.current_device())
+        sampler.start()
+        t, ts = graph_timed_apply(torch, op, u, y, dirichlet, flush, K)
+        tb = []                                   # burst: one apply after an idle, synchronised GPU
+        for k in range(5):
             flush.fill_(float(k))
+            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             op.apply(u, y, dirichlet=dirichlet)
             e1.record(stream)
             e1.synchronize()
-            ts.append(e0.elapsed_time(e1) * 1e-3)
-        t = float(np.median(ts))
+            tb.append(e0.elapsed_time(e1) * 1e-3)
         b = op.load_vector(1.0, dirichlet=dirichlet)
         x = torch.zeros_like(b)
         op.cg(b, x, maxit=-3, dirichlet=dirichlet)
-        r = op.cg(b, x, maxit=-K, dirichlet=dirichlet, resume=True)
+        op.cg(b, x, rtol=0.0, maxit=K, dirichlet=dirichlet, resume=True)     # builds the CG graph
+        r = op.cg(b, x, rtol=0.0, maxit=K, dirichlet=dirichlet, resume=True)  # K iterations, one graph
+        clk = sampler.stop()
         ab = alg_bytes(oi, c.n_elem, c.ndof)
         fl = oi["flops_per_elem"] * c.n_elem
+        t_burst = float(np.min(tb))
         rows.append({"config": name, "storage": storage, "form": "EL" if form == 1 else "WP", "d": c.d, "N": c.N,
                      "p": c.p, "ndof": c.ndof, "n_elem": c.n_elem, "dirichlet": dirichlet,
                      "apply_ms": t * 1e3, "apply_ms_min": min(ts) * 1e3, "GDoF_s": c.ndof / t / 1e9,
+                     "apply_ms_burst": t_burst * 1e3, "frac_measured_hbm_burst": ab / t_burst / 1e9 / peak,
+                     "clocks": clk,
                      "alg_bytes": ab, "achieved_GBs": ab / t / 1e9, "frac_measured_hbm": ab / t / 1e9 / peak,
                      "frac_8TBs": ab / t / 8e12, "fp64_TFs": fl / t / 1e12,
                      "fp64_frac_measured_dfma": fl / t / 1e12 / FP64_PEAK_TFLOPS,
-                     "cg_ms_per_iter": r["seconds"] / K * 1e3, "weights_ms": oi["weights_ms"],
-                     "l2": "flushed (256 MB write) before each timed apply; CG iterations back to back",
+                     "cg_ms_per_iter": r["seconds"] / max(1, r["iters"]) * 1e3, "cg_iters_timed": r["iters"],
+                     "weights_ms": oi["weights_ms"],
+                     "l2": "flushed (256 MB write) before each timed apply; apply_ms: CUDA-graph replay of K x "
+                           "(flush, apply) minus K x (flush), sustained back to back, no host launch gaps; "
+                           "apply_ms_burst: best of 5 single applies after a synchronised idle GPU (includes "
+                           "the host launch gap, matters for the us-scale configs); CG: K iterations back "
+                           "to back in the single-rank CG graph (dogip_cg, rtol 0)",
                      "setup_s": time.perf_counter() - t0})
         op.close()
         m.close()

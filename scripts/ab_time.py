@@ -11,6 +11,7 @@ import torch  # noqa: E402
 
 from paper_1710_09913_b200.api import Mesh, Operator  # noqa: E402
 from synth.configs import get_config  # noqa: E402
+from bench import graph_timed_apply  # noqa: E402
 
 CODE = {"full": 0, "iso": 1, "global": 2, "qp": 4, "sym": 5}
 K = int(os.environ.get("AB_K", "15"))
@@ -25,16 +26,8 @@ for spec in sys.argv[1:]:
     y = torch.empty_like(u)
     for _ in range(3):
         op.apply(u, y, dirichlet=form == 1)
-    ts = []
-    for k in range(K):
-        flush.fill_(float(k))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        op.apply(u, y, dirichlet=form == 1)
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    print(f"{os.path.basename(os.environ.get('DOGIP_LIB', 'base'))} {spec:12s} apply {np.median(ts):.4f} ms "
-          f"(min {min(ts):.4f})", flush=True)
+    t, ts = graph_timed_apply(torch, op, u, y, form == 1, flush, K)
+    print(f"{os.path.basename(os.environ.get('DOGIP_LIB', 'base'))} {spec:12s} apply {t * 1e3:.4f} ms "
+          f"(min {min(ts) * 1e3:.4f}; CUDA-graph replay, L2 flushed)", flush=True)
     op.close()
     m.close()
