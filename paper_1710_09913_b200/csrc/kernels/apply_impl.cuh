@@ -81,7 +81,9 @@ constexpr int min_blocks() {
 #ifdef DOGIP_MINB_OVERRIDE
     return DOGIP_MINB_OVERRIDE;
 #endif
-    return RE::VT <= 10 ? DOGIP_MINB_SMALL : RE::VT <= 20 ? 3 : DOGIP_MINB_LARGE;
+    // 2D P4 (V_T = 15): 2 CTAs / 255 registers beat 3 / 168 with spills (C2 p=4 -4 %, iso -5 %,
+    // profiles/r02_ab_minb.log)
+    return RE::VT <= 10 ? DOGIP_MINB_SMALL : (RE::VT <= 20 && RE::NS == 6) ? 3 : DOGIP_MINB_LARGE;
 }
 
 // Balanced chunks of whole nodes: NCH = ceil(TILE_ROWS / ROWS_MAX) chunks of ROWS rows
@@ -100,9 +102,13 @@ constexpr int min_blocks() {
 // -5 % for the FP64-bound ISO storage (C4 iso 2.47 -> 2.34 ms, C2 p=4 iso -14 %), -1 % for
 // the long full tiles of C4 / C5; +3 % for the symmetry-adapted kernel, +2 % for C2 p=4 EL
 template <class RE>
+struct LockstepPolicy {
+    static constexpr bool value = !RE::DOT_IN_BODY && (RE::NG > 0 || RE::TILE_ROWS >= 165);
+};
+template <class RE>
 __host__ __device__ constexpr bool lockstep() {
     if constexpr (DOGIP_LOCKSTEP >= 0) return DOGIP_LOCKSTEP != 0;
-    else return !RE::DOT_IN_BODY && (RE::NG > 0 || RE::TILE_ROWS >= 165);
+    else return LockstepPolicy<RE>::value;
 }
 
 template <class RE, int TW = TILE>
@@ -507,13 +513,23 @@ struct CellRE {     // the ns element tiles of one cell tile, read as one super 
         return (J / RE::WT) * RE::TILE_ROWS + RE::row_of(J % RE::WT);
     }
 };
+#ifndef DOGIP_CELL_LOCKSTEP
+#define DOGIP_CELL_LOCKSTEP 0   // C3 (3D P2) cell kernel: 24 % of stall samples at the lockstep barrier
+#endif
+template <class RE>
+struct LockstepPolicy<CellRE<RE>> {
+    static constexpr bool value = DOGIP_CELL_LOCKSTEP != 0 && LockstepPolicy<RE>::value;
+};
 
+#ifndef DOGIP_CELL_MAXP_2D
+#define DOGIP_CELL_MAXP_2D 3   // 2D: cells of up to (p+1)^2 = 16 DoFs per lane (P4 spills: slower)
+#endif
 template <int D, int P>
 __host__ __device__ constexpr bool cell_kernel_enabled() {
 #ifdef DOGIP_NO_CELL_KERNEL
     return false;
 #else
-    return P <= 2;
+    return P <= 2 || (D == 2 && P <= DOGIP_CELL_MAXP_2D);
 #endif
 }
 
@@ -704,12 +720,15 @@ __device__ __forceinline__ void cell_scatter(double* __restrict__ y, const doubl
             }
 }
 
+#ifndef DOGIP_CELL_MINB_2D1
+#define DOGIP_CELL_MINB_2D1 8   // 2D P1: <= 64 registers, 32 warps per SM (latency-bound gathers)
+#endif
 #ifndef DOGIP_CELL_MINB_3D2
 #define DOGIP_CELL_MINB_3D2 2   // 3D P2: 27 + 27 cell values per lane (3 CTAs/SM spills)
 #endif
 template <int D, int P>
 constexpr int cell_min_blocks() {
-    return (D == 3 && P == 2) ? DOGIP_CELL_MINB_3D2 : 3;
+    return (D == 3 && P == 2) ? DOGIP_CELL_MINB_3D2 : (D == 2 && P == 4) ? 2 : (D == 2 && P == 1) ? DOGIP_CELL_MINB_2D1 : 3;
 }
 
 template <int D, int P, int F, bool DIR>

@@ -707,10 +707,10 @@ def test_slab_partials_every_storage(d, N, p, form, nr):
                 i0 = m.info["dof_offset"]
                 ul = torch.from_numpy(u[i0:i0 + m.ndof].copy()).cuda()
                 acc[i0:i0 + m.ndof] += op.apply(ul, exchange=False, dirichlet=dirichlet).cpu().numpy()
-            if dirichlet and not (store == 0 and p <= 2):
+            if dirichlet and not (store == 0 and (p <= 2 or (d == 2 and p <= 3))):
                 # the separate fix-up writes the Dirichlet rows (u_i) of the interface planes
-                # on both owners: count them once.  The cell kernel (FULL storage, p <= 2)
-                # writes each row once (its floor cell), so its partials already sum to u_i.
+                # on both owners: count them once.  The cell kernel (FULL storage; p <= 2, 2D
+                # p <= 3) writes each row once (its floor cell): partials already sum to u_i.
                 mask = boundary_mask(d, N, p)
                 plane = Md ** (d - 1)
                 for r in range(1, nr):
