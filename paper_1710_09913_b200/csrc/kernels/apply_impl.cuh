@@ -329,10 +329,11 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     using C = Chunking<RE>;
     constexpr int NW = APPLY_THREADS / 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    constexpr bool RING = !(GLOB || direct_weights<RE>());                   // weight ring + mbarriers
     double* rings = reinterpret_cast<double*>(smem_raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)NW * C::S * C::ROWS * TILE);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (RING ? (size_t)NW * C::S * C::ROWS * TILE : 0));
     constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
-    double* ubufs = reinterpret_cast<double*>(bars + NW * C::S);            // [NW][VT][32] (UPF only)
+    double* ubufs = reinterpret_cast<double*>(bars + (RING ? NW * C::S : 0));   // [NW][VT][32] (UPF only)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw = tile_begin + (int64_t)blockIdx.x * NW + warp;
@@ -471,8 +472,8 @@ cudaError_t launch_one(const ApplyArgs& a) {
     constexpr int NW = APPLY_THREADS / 32;
     constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
     constexpr bool DW = direct_weights<RE>() && !GLOB;
-    const size_t smem = (GLOB || DW) ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8 +
-                                   (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0);
+    const size_t smem = ((GLOB || DW) ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8) +
+                        (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0);
     auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
     static std::atomic<uint64_t> cfg[MAX_DEVICES];   // per instantiation, per device
     int occ = 1;
