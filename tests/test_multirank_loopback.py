@@ -174,3 +174,46 @@ def test_loopback_partials_without_exchange_and_group_lifetime():
     for m in meshes:
         m.close()
     group.close()
+
+
+_DEAD_PEER = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_1710_09913_b200.api import DogipError, LoopbackGroup, Mesh, Operator
+from synth.configs import COEF_CONST, Coefficient
+g = LoopbackGroup(2, device=0)
+ms = [Mesh(3, 4, 2, rank=r, nranks=2, device=0, loopback=g) for r in range(2)]
+ops = [Operator(m, 1, Coefficient(COEF_CONST, np.array([1.0]))) for m in ms]
+u = torch.zeros(ms[0].ndof, dtype=torch.float64, device="cuda")
+try:                                   # rank 1 never calls: rank 0 must not hang
+    ops[0].apply(u)
+    print("NO_ERROR")
+except DogipError as e:
+    print("RANK0", e.code, str(e))
+try:                                   # the group is dead: rank 1 fails at once
+    ops[1].apply(torch.zeros(ms[1].ndof, dtype=torch.float64, device="cuda"))
+    print("NO_ERROR")
+except DogipError as e:
+    print("RANK1", e.code, str(e))
+"""
+
+
+def test_dead_peer_times_out_instead_of_hanging():
+    """A rank whose neighbour never joins the collective gets E_NCCL after
+    DOGIP_COMM_TIMEOUT_S instead of hanging, and the communicator is then dead for every
+    rank (include/dogip.h dogip_apply / dogip_cg error behaviour)."""
+    import os
+    import subprocess
+    import sys
+    import time
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DOGIP_COMM_TIMEOUT_S="2")
+    t0 = time.time()
+    r = subprocess.run([sys.executable, "-c", _DEAD_PEER.format(root=root)], capture_output=True, text=True,
+                       timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = {l.split()[0]: l for l in r.stdout.splitlines() if l.startswith("RANK")}
+    assert "NO_ERROR" not in r.stdout
+    assert lines["RANK0"].split()[1] == "-8" and "timeout" in lines["RANK0"]
+    assert lines["RANK1"].split()[1] == "-8" and "dead" in lines["RANK1"]
+    assert time.time() - t0 < 200
