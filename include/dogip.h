@@ -305,7 +305,8 @@ int dogip_load_vector(dogip_op op, double f, double* b, unsigned flags, void* st
  * (several ranks, or DOGIP_CG_NO_GRAPH=1) batches of DOGIP_CG_BATCH (default 32)
  * iterations are enqueued at once and the host reads the device's done flag once
  * per batch; iterations enqueued after the stop are no-ops (the apply kernel returns
- * at once).  With a communicator every wait polls its asynchronous error state: a
+ * at once).  With an NCCL communicator and DOGIP_CG_GRAPH_MR=1 a batch, NCCL calls
+ * included, is captured once as a CUDA graph and replayed.  With a communicator every wait polls its asynchronous error state: a
  * dead peer or no progress within DOGIP_COMM_TIMEOUT_S seconds (default 600) aborts
  * the communicator and returns E_NCCL.
  */

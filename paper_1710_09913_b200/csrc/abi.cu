@@ -95,6 +95,10 @@ struct dogip_op_s {
     cudaGraph_t cg_graph = nullptr;
     cudaGraphExec_t cg_exec = nullptr;
     cudaStream_t cap_stream = nullptr;   // capture stream (the legacy default stream cannot capture)
+    // several ranks (DOGIP_CG_GRAPH_MR=1, capturable communicator): a batch of predicated
+    // iterations, NCCL calls included, as one CUDA graph
+    cudaGraphExec_t mr_exec = nullptr;
+    struct { const double* x = nullptr; unsigned flags = 0; double rtol = 0.0; int maxit = 0, batch = 0; cudaStream_t st = nullptr; } mr_key;
     struct { const double* x = nullptr; unsigned flags = 0; double rtol = 0.0; int maxit = 0; cudaStream_t st = nullptr; } cg_key;
     // pipelined host-buffer apply: copy-in / copy-out streams, one event pair per chunk
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
@@ -677,6 +681,7 @@ extern "C" void dogip_op_destroy(dogip_op op) {
     for (double* x : {op->q_pts, op->q_wts, op->q_phi, op->q_dphi, op->q_params, op->q_cell}) cudaFree(x);
     if (op->h_scal) cudaFreeHost(op->h_scal);
     if (op->cg_exec) cudaGraphExecDestroy(op->cg_exec);
+    if (op->mr_exec) cudaGraphExecDestroy(op->mr_exec);
     if (op->cg_graph) cudaGraphDestroy(op->cg_graph);
     if (op->cap_stream) cudaStreamDestroy(op->cap_stream);
     for (cudaEvent_t e : op->ev_in) cudaEventDestroy(e);
@@ -972,6 +977,36 @@ static int cg_graph_build(dogip_op op, double* x, double rtol, int maxit, unsign
     return DOGIP_OK;
 }
 
+// Several ranks: `batch` predicated iterations -- exchange and all-reduces of the
+// communicator included -- captured once as a plain CUDA graph (opt-in, DOGIP_CG_GRAPH_MR=1;
+// validated with a 1-rank NCCL communicator on the one-GPU pool).  Rebuilt when x, the flags,
+// rtol, maxit, the batch or the stream change.
+static int cg_batch_graph_build(dogip_op op, double* x, double rtol, int maxit, unsigned aflags, cudaStream_t st,
+                                int batch) {
+    auto& k = op->mr_key;
+    if (op->mr_exec && k.x == x && k.flags == aflags && k.rtol == rtol && k.maxit == maxit && k.batch == batch &&
+        k.st == st)
+        return DOGIP_OK;
+    if (op->mr_exec) { cudaGraphExecDestroy(op->mr_exec); op->mr_exec = nullptr; }
+    if (!op->cap_stream) CK(cudaStreamCreateWithFlags(&op->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t cs = op->cap_stream;
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int rc = DOGIP_OK;
+    for (int i = 0; i < batch && rc >= 0; ++i) rc = cg_iteration(op, x, aflags, rtol, maxit, nullptr, cs);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(cs, &g);
+    if (rc < 0) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    CK(ee);
+    const cudaError_t ie = cudaGraphInstantiate(&op->mr_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) { op->mr_exec = nullptr; CK(ie); }
+    k.x = x; k.flags = aflags; k.rtol = rtol; k.maxit = maxit; k.batch = batch; k.st = st;
+    return DOGIP_OK;
+}
+
 extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, int maxit, unsigned flags,
                         void* stream, dogip_cg_result* res) {
     if (!op || !res) return fail(DOGIP_E_INVALID_ARG, "null argument");
@@ -1019,6 +1054,11 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
     // single rank: the graph-captured loop is built (or reused) before the timed region
     const bool graph = !bench && nit > 0 && !m->comm && std::getenv("DOGIP_CG_NO_GRAPH") == nullptr;
     if (graph) RET(cg_graph_build(op, x, rtol_dev, nit, aflags, st));
+    int batch = 32;
+    if (const char* e = std::getenv("DOGIP_CG_BATCH")) batch = std::max(1, std::atoi(e));
+    const char* mre = std::getenv("DOGIP_CG_GRAPH_MR");
+    const bool mr_graph = !bench && nit > 0 && m->comm && m->comm->capturable() && mre && mre[0] == '1';
+    if (mr_graph) RET(cg_batch_graph_build(op, x, rtol_dev, nit, aflags, st, batch));
     CK(cudaEventRecord(t0, st));
     if (!resume) {
         // r = b - A x ; p = r
@@ -1044,12 +1084,12 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
             if (graph) {
                 CK(cudaGraphLaunch(op->cg_exec, st));
             } else {
-                // eagerly enqueued batches of predicated iterations, one host read per batch
-                int batch = 32;
-                if (const char* e = std::getenv("DOGIP_CG_BATCH")) batch = std::max(1, std::atoi(e));
+                // batches of predicated iterations (eager, or one captured graph per batch),
+                // one host read of the device's done flag per batch
                 for (int enq = 0; enq < nit;) {
-                    const int kk = std::min(batch, nit - enq);
-                    for (int i = 0; i < kk; ++i) RET(cg_iteration(op, x, aflags, rtol_dev, nit, nullptr, st));
+                    const int kk = mr_graph ? batch : std::min(batch, nit - enq);
+                    if (mr_graph) CK(cudaGraphLaunch(op->mr_exec, st));
+                    else for (int i = 0; i < kk; ++i) RET(cg_iteration(op, x, aflags, rtol_dev, nit, nullptr, st));
                     enq += kk;
                     CK(cudaMemcpyAsync(op->h_scal, op->scal, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost, st));
                     RET(stream_sync(m, st));

@@ -916,3 +916,39 @@ def test_plain_dogip_weights_entry_point(form):
     lib.dogip_op_destroy(h)
     ref.close()
     m.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,N,p,form", [(3, 5, 2, 1), (2, 40, 2, 0)])
+def test_nccl_cg_batch_graph(d, N, p, form):
+    """Several-rank CG through a 1-rank NCCL communicator: eager batches of predicated
+    iterations and the opt-in captured batch graph (DOGIP_CG_GRAPH_MR=1, NCCL calls inside
+    the graph), with batches shorter than the solve, give the single-rank graph's solve."""
+    import os
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator, nccl_unique_id
+    coef = Coefficient(COEF_CONST, np.array([1.3]))
+    dirichlet = form == 1
+    m0 = Mesh(d, N, p, device=0)
+    op0 = Operator(m0, form, coef)
+    b = op0.load_vector(1.0, dirichlet=dirichlet)
+    x0 = torch.zeros_like(b)
+    r0 = op0.cg(b, x0, rtol=1e-10, dirichlet=dirichlet)
+    m1 = Mesh(d, N, p, nranks=1, nccl_id=nccl_unique_id(), device=0)
+    op1 = Operator(m1, form, coef)
+    for env in ({"DOGIP_CG_BATCH": "7"}, {"DOGIP_CG_BATCH": "7", "DOGIP_CG_GRAPH_MR": "1"},
+                {"DOGIP_CG_GRAPH_MR": "1"}):
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            x1 = torch.zeros_like(b)
+            r1 = op1.cg(b, x1, rtol=1e-10, dirichlet=dirichlet)
+        finally:
+            for k, v in old.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        assert r1["status"] == r0["status"] == "OK", (env, r1)
+        assert abs(r1["iters"] - r0["iters"]) <= 2, (env, r1["iters"], r0["iters"])
+        assert relerr(x1.cpu().numpy(), x0.cpu().numpy()) <= 1e-8, env
