@@ -952,3 +952,43 @@ def test_nccl_cg_batch_graph(d, N, p, form):
         assert r1["status"] == r0["status"] == "OK", (env, r1)
         assert abs(r1["iters"] - r0["iters"]) <= 2, (env, r1["iters"], r0["iters"])
         assert relerr(x1.cpu().numpy(), x0.cpu().numpy()) <= 1e-8, env
+
+
+_ELEMENT_PATH = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from oracle import assemble as oa
+from oracle.mesh import boundary_mask
+from paper_1710_09913_b200.api import Mesh, Operator
+from synth.configs import COEF_CONST, Coefficient
+from synth.generators import u_vector
+worst = 0.0
+for d, N, p in [(2, 34, 1), (2, 33, 2), (2, 9, 3), (3, 3, 1), (3, 3, 2)]:
+    for form in (0, 1):
+        coef = Coefficient(COEF_CONST, np.array([1.4]))
+        ed = oa.build(d, N, p)
+        A = oa.assemble_csr(ed, form, coef)
+        AD = oa.dirichlet_matrix(A, boundary_mask(d, N, p))
+        u = u_vector(ed.ndof, 4)
+        op = Operator(Mesh(d, N, p, device=0), form, coef)
+        ut = torch.from_numpy(u).cuda()
+        for dirichlet, ref in ((False, A @ u), (True, AD @ u)):
+            y = op.apply(ut, dirichlet=dirichlet).cpu().numpy()
+            worst = max(worst, np.abs(y - ref).max() / np.abs(ref).max())
+print("WORST", worst)
+"""
+
+
+@pytest.mark.gpu
+def test_element_kernel_path_for_small_p():
+    """DOGIP_CELL_KERNEL=0 routes FULL storage with p <= 2 (2D p <= 3) to the element-per-lane
+    kernel (the cell kernel's fallback); it stays parity-green."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _ELEMENT_PATH.format(root=root)], capture_output=True, text=True,
+                       timeout=600, env=dict(os.environ, DOGIP_CELL_KERNEL="0"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    worst = float([l for l in r.stdout.splitlines() if l.startswith("WORST")][0].split()[1])
+    assert worst <= TOL, worst
