@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: no-op unless a profiler is attached
+
 #include "../../include/dogip.h"
 #include "host/comm.hpp"
 #include "host/quadrature.hpp"
@@ -53,6 +55,12 @@ static int fail(int code, const std::string& msg) {
         int rc_ = (call);             \
         if (rc_ < 0) return rc_;      \
     } while (0)
+
+// host-side NVTX range for the duration of an entry point (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ handles
 struct dogip_mesh_s {
@@ -454,6 +462,7 @@ extern "C" int dogip_weights(dogip_mesh m, int form, const dogip_coeff* coeff, i
 
 extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff, int quad_n1d, int storage,
                                 void* stream, dogip_op* out) {
+    NvtxRange nv("dogip_weights");
     if (!m || !out) return fail(DOGIP_E_INVALID_ARG, "null argument");
     *out = nullptr;
     if (form != DOGIP_WP && form != DOGIP_EL) return fail(DOGIP_E_INVALID_ARG, "form must be DOGIP_WP or DOGIP_EL");
@@ -693,6 +702,7 @@ extern "C" void dogip_op_destroy(dogip_op op) {
 
 // ------------------------------------------------------------------ apply
 static int exchange_planes(dogip_mesh_s* m, double* y, cudaEvent_t ready) {
+    NvtxRange nv("dogip_exchange");
     // sum this rank's partial interface planes with the neighbours' (A8)
     const int64_t P = m->d == 3 ? m->geo.sy * m->geo.sy : m->geo.sy;
     const int64_t last = m->geo.ndof - P;
@@ -796,6 +806,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
 }
 
 extern "C" int dogip_apply(dogip_op op, const double* u, double* y, unsigned flags, void* stream) {
+    NvtxRange nv("dogip_apply");
     if (!op) return fail(DOGIP_E_INVALID_ARG, "null argument");
     RET(check_vec(u, "u"));
     RET(check_vec(y, "y"));
@@ -876,6 +887,7 @@ static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_hos
 }
 
 extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_host, unsigned flags, void* stream) {
+    NvtxRange nv("dogip_apply_host");
     if (!op || !u_host || !y_host) return fail(DOGIP_E_INVALID_ARG, "null argument");
     if (flags & ~(DOGIP_DIRICHLET_ZERO | DOGIP_NO_EXCHANGE)) return fail(DOGIP_E_INVALID_ARG, "unknown flags");
     cudaStream_t st = (cudaStream_t)stream;
@@ -895,6 +907,7 @@ extern "C" int dogip_apply_host(dogip_op op, const double* u_host, double* y_hos
 }
 
 extern "C" int dogip_load_vector(dogip_op op, double f, double* b, unsigned flags, void* stream) {
+    NvtxRange nv("dogip_load_vector");
     if (!op) return fail(DOGIP_E_INVALID_ARG, "null argument");
     RET(check_vec(b, "b"));
     RET(comm_check(op->m));
@@ -1009,6 +1022,7 @@ static int cg_batch_graph_build(dogip_op op, double* x, double rtol, int maxit, 
 
 extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, int maxit, unsigned flags,
                         void* stream, dogip_cg_result* res) {
+    NvtxRange nv("dogip_cg");
     if (!op || !res) return fail(DOGIP_E_INVALID_ARG, "null argument");
     RET(check_vec(b, "b"));
     RET(check_vec(x, "x"));
