@@ -218,8 +218,9 @@ int dogip_mesh_setup(int d, int64_t N, int p, const double* vertices, int rank, 
 int dogip_mesh_setup_ex(int d, int64_t N, int p, const double* vertices, int rank, int nranks,
                         int comm_kind, const void* comm_arg, int device, dogip_mesh* out);
 
-/* In-process loopback group of nranks ranks on `device` (DOGIP_COMM_LOOPBACK).  Destroy
- * after every mesh using it (else E_INVALID_ARG). */
+/* In-process loopback group of nranks ranks on `device` (DOGIP_COMM_LOOPBACK): serves ONE
+ * mesh per rank (the ranks' collectives are matched by call order).  Destroy after every
+ * mesh using it (else E_INVALID_ARG). */
 int dogip_loopback_create(int nranks, int device, dogip_loopback* out);
 int dogip_loopback_destroy(dogip_loopback group);
 
