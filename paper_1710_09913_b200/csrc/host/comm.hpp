@@ -182,7 +182,7 @@ struct LoopbackGroup {
     double* slots = nullptr;             // [2][nranks][SLOT] device scratch of the all-reduce
     static constexpr int64_t SLOT = 64;
     int members = 0;                     // meshes attached
-    bool destroy_requested = false;
+    std::vector<char> rank_used;         // one mesh per rank (collectives match by call order)
 
     // wait (host) until pred() holds; false on timeout or a dead group
     template <class Pred>
@@ -216,10 +216,15 @@ public:
         g = grp;
         rank = r;
         nranks = n;
+        {
+            std::lock_guard<std::mutex> lk(g->mu);
+            if ((int)g->rank_used.size() < n) g->rank_used.resize(n, 0);
+            if (g->rank_used[r]) { g = nullptr; return bad(-10, "loopback group already has a mesh for this rank"); }
+            g->rank_used[r] = 1;
+            ++g->members;
+        }
         for (cudaEvent_t* e : {&ev_send, &ev_done, &ev_ar})
             if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return bad(-7, "event create");
-        std::lock_guard<std::mutex> lk(g->mu);
-        ++g->members;
         return 0;
     }
     ~LoopbackComm() override {
@@ -228,6 +233,7 @@ public:
         if (g) {
             std::lock_guard<std::mutex> lk(g->mu);
             --g->members;
+            g->rank_used[rank] = 0;
         }
     }
     int exchange(const double* lo_send, const double* hi_send, double* lo_recv, double* hi_recv, int64_t P,

@@ -515,11 +515,12 @@ struct CellRE {     // the ns element tiles of one cell tile, read as one super 
     }
 };
 #ifndef DOGIP_CELL_LOCKSTEP
-#define DOGIP_CELL_LOCKSTEP 0   // C3 (3D P2) cell kernel: 24 % of stall samples at the lockstep barrier
+#define DOGIP_CELL_LOCKSTEP -1  // -1: 2D cell kernels lock-step (C2 p=3 -3 %), 3D do not (C3 neutral,
+                                // 24 % of its stall samples sat at the barrier); 0 / 1 force (A/B)
 #endif
 template <class RE>
 struct LockstepPolicy<CellRE<RE>> {
-    static constexpr bool value = DOGIP_CELL_LOCKSTEP != 0 && LockstepPolicy<RE>::value;
+    static constexpr bool value = DOGIP_CELL_LOCKSTEP >= 0 ? DOGIP_CELL_LOCKSTEP != 0 : RE::NS == 2;
 };
 
 #ifndef DOGIP_CELL_MAXP_2D

@@ -171,6 +171,8 @@ def test_loopback_partials_without_exchange_and_group_lifetime():
     assert np.abs(acc - y).max() <= 1e-13 * np.abs(y).max()
     with pytest.raises(DogipError):
         group.close()
+    with pytest.raises(DogipError):                  # one mesh per rank and group
+        Mesh(d, N, p, rank=1, nranks=nr, device=0, loopback=group)
     for m in meshes:
         m.close()
     group.close()
