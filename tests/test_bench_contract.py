@@ -43,3 +43,25 @@ def test_product_arm_contract():
     assert d["gpu_launches"] > 0 and d["value"] > 0 and d["ms_per_step"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == d["e2e"]["d2h_bytes_per_step"] == 8 * 33 * 33
     assert d["dtype"] == "f64" and d["n_gpus"] == 1
+
+
+@pytest.mark.gpu
+def test_product_arm_multirank_code_path():
+    """--dist: the bench's multi-rank branch (process group, NCCL id broadcast, the library's
+    NCCL communicator, exchange + all-reduced CG, max over ranks) through a 1-rank group."""
+    d = _run(["--config", "C1", "--steps", "2", "--warmup", "1", "--no-cpu-baseline", "--no-variants", "--dist"])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["ms_per_step"] > 0
+    assert d["gpu_launches"] > 0 and 0 < d["roofline"]["frac"]
+
+
+def test_gpus_flag_without_enough_devices_fails_clearly():
+    """--gpus N outside torchrun self-launches N ranks, or exits non-zero with a clear message
+    when fewer than N GPUs are visible (never silently times one GPU)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64", "--config", "C1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode != 0
+    assert "needs 64 visible GPUs" in r.stderr
+    env = dict(os.environ, WORLD_SIZE="2")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--config", "C1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr
