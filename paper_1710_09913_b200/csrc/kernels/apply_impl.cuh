@@ -26,6 +26,11 @@
 //    scattered with fire-and-forget red.global.add.f64 (y zeroed first), so the
 //    gather latency overlaps the scatter; DIRICHLET zeroes boundary DoFs of u_T
 //    and skips their scatter (the boundary rows are fixed by dirichlet_fixup).
+// Kernels in this file:
+//  * apply_kernel       element per lane (above): p >= 3 (2D p = 4), ISO, SYM, GLOBAL;
+//  * apply_cell_kernel  cell per lane (all d! simplices of a cell, DoFs shared on chip,
+//                       x faces by shuffles, Dirichlet rows written in-kernel): FULL storage,
+//                       p <= 2 and 2D p = 3 (see "cell per lane" below).
 #pragma once
 #include <cuda_runtime.h>
 
