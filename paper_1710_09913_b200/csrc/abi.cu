@@ -252,6 +252,7 @@ extern "C" int dogip_mesh_setup_ex(int d, int64_t N, int p, const double* vertic
     g.swy = MW;
     g.swz = d == 3 ? MW * MW : 0;
     g.ndof_w = ipow(MW, d - 1) * (2 * p * L + 1);
+    g.rw = 2 * p * ((int64_t)g.Nx + 1);
     for (int s = 0; s < g.ns; ++s)
         for (int l = 0; l < m->ref.VT; ++l) {
             const int* o = m->ref.loff[s][l];
@@ -659,6 +660,25 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
         if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
         cudaFree(cnt);
         if (ce != cudaSuccess) return cleanup_fail(DOGIP_E_CUDA, std::string("globalize: ") + cudaGetErrorString(ce));
+        // class-major layout for coalesced gathers: rows of the W lattice (y, z) of length
+        // 2p (Nx+1); node offsets re-expressed in it
+        const int64_t rows = m->geo.ndof_w / MW;
+        double* wp = nullptr;
+        if (cudaMalloc(&wp, sizeof(double) * rows * m->geo.rw) != cudaSuccess)
+            return cleanup_fail(DOGIP_E_OOM, "global W weights (class-major)");
+        cudaMemsetAsync(wp, 0, sizeof(double) * rows * m->geo.rw, st);
+        ce = launch_permute_w(m->geo, wg, wp, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        cudaFree(wg);
+        op->d_w = wp;
+        op->w_doubles = rows * m->geo.rw;
+        if (ce != cudaSuccess) return cleanup_fail(DOGIP_E_CUDA, std::string("permute W: ") + cudaGetErrorString(ce));
+        const int twop = 2 * p;
+        for (auto& o : offw) {
+            const int64_t ox = o % MW, oy = (o / MW) % MW, oz = d == 3 ? o / (MW * MW) : 0;
+            o = (int)(m->geo.rw * (oy + MW * oz) + (ox % twop) * (m->geo.Nx + 1) + ox / twop);
+        }
+        cudaMemcpy(op->d_offw, offw.data(), sizeof(int) * offw.size(), cudaMemcpyHostToDevice);
     }
     *out = op;
     return DOGIP_OK;
@@ -1279,7 +1299,7 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
             if (e < 0) continue;
             if (op->store == DOGIP_STORE_GLOBAL) {     // the global weights each element sees
                 const TileCoord tc = tile_coord(g, t);
-                const int64_t bw = (int64_t)(2 * g.p) * (tc.ci0 + lane + g.swy * tc.cj + g.swz * tc.ck);
+                const int64_t bw = g.rw * (int64_t)(2 * g.p) * (tc.cj + g.swy * tc.ck) + tc.ci0 + lane;
                 for (int j = 0; j < WT; ++j) host[e * WT + j] = w[bw + offw[(size_t)tc.s * WT + j]];
                 continue;
             }

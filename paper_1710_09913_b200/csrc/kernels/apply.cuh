@@ -127,6 +127,8 @@ cudaError_t launch_weights(const WeightsArgs& a);
 cudaError_t launch_divide(double* a, const double* b, int64_t n, cudaStream_t st);
 cudaError_t launch_globalize(const SlabGeo& g, int WT, const double* wel, const int* offw, double* wg,
                              cudaStream_t st);
+// natural W lattice -> the class-major layout the apply reads (geo.rw; padding left untouched)
+cudaError_t launch_permute_w(const SlabGeo& g, const double* nat, double* out, cudaStream_t st);
 
 // ----------------------------------------------------------- quadrature-point comparator
 // Matrix-free A u over the integration points, no stored operator.

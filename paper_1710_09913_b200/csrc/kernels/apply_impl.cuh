@@ -233,7 +233,9 @@ __device__ __forceinline__ void lockstep_tail(int64_t gw, int64_t tile_end, int6
 }
 
 // Theorem 1 storage (global WP diagonal over W = C_{N,2p}): the weight of
-// double-grid node j of the element is gathered from the global W-lattice vector.
+// double-grid node j of the element is gathered from the global W-lattice vector, stored
+// class-major along x (x = 2p c + k at k (Nx+1) + c), so a tile's 32 lanes read 32
+// consecutive doubles per node; offw holds each node's offset in that layout.
 struct GatherPol {
     const double* wg;      // global W weights of this slab
     const int* offw;       // shared-memory W-lattice offsets of this simplex type
@@ -442,7 +444,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
         for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
         if constexpr (GLOB) {
             GatherPol gp{w, offw_s + cur.s * MAX_WT_GLOBAL,
-                         (int64_t)(2 * geo.p) * (cur.ci + geo.swy * cur.cj + geo.swz * cur.ck)};
+                         geo.rw * (int64_t)(2 * geo.p) * (cur.cj + geo.swy * cur.ck) + cur.ci};
             RE::body(uT, yT, gp);
         } else {
             if constexpr (RE::DOT_IN_BODY) RE::body(uT, yT, ws, dot_partials ? &udot : nullptr);

@@ -42,6 +42,7 @@ struct SlabGeo {
     int N;                         // global cells per axis
     int64_t swy, swz;              // W-lattice (order 2p) strides of the global WP storage
     int64_t ndof_w;                // local W-lattice DoFs
+    int64_t rw;                    // stored row length of the class-major W layout: 2p (Nx + 1)
     FastDiv fd_ns, fd_nxb, fd_ny;  // divisors of tile_coord (set with the fields above)
 };
 

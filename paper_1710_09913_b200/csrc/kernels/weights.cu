@@ -272,6 +272,17 @@ __global__ void globalize_kernel(SlabGeo g, int WT, const double* __restrict__ w
         red_add_f64(wg + base + offw[tc.s * WT + j], wel ? wel[((size_t)tile * WT + j) * TILE + lane] : 1.0);
 }
 
+// natural W lattice (x fastest) -> class-major rows: x = 2p c + k stored at k (Nx+1) + c,
+// so the 32 lanes of a tile (cells c .. c+31) read 32 consecutive doubles for every W node
+__global__ void permute_w_kernel(SlabGeo g, const double* __restrict__ nat, double* __restrict__ out) {
+    const int64_t MW = g.swy, twop = 2 * g.p;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.ndof_w; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / MW, x = i - row * MW;
+        const int64_t cc = x / twop, k = x - cc * twop;
+        out[row * g.rw + k * (g.Nx + 1) + cc] = nat[i];
+    }
+}
+
 __global__ void divide_kernel(double* a, const double* b, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         a[i] = b[i] > 0.0 ? a[i] / b[i] : 0.0;
@@ -282,6 +293,14 @@ cudaError_t launch_divide(double* a, const double* b, int64_t n, cudaStream_t st
     int64_t blocks = (n + 255) / 256;
     if (blocks > 4 * 148 * 8) blocks = 4 * 148 * 8;
     divide_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, b, n);
+    count_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_permute_w(const SlabGeo& g, const double* nat, double* out, cudaStream_t st) {
+    int64_t blocks = (g.ndof_w + 255) / 256;
+    if (blocks > 4 * 148 * 8) blocks = 4 * 148 * 8;
+    permute_w_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, nat, out);
     count_launches(1);
     return cudaGetLastError();
 }

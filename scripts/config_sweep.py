@@ -106,7 +106,7 @@ def main():
         if args.iso and 0 in forms and c.p <= 4:
             variants.append((0, 2))
         if args.iso and 0 in forms:
-            variants += [(0, 3), (0, 5)]
+            variants += [(0, 5)]
         if args.qp:
             variants += [(f, 4) for f in forms]
         for form, storage in variants:
@@ -129,7 +129,7 @@ def main():
             x = torch.zeros_like(b)
             op.cg(b, x, maxit=-3, dirichlet=dirichlet)
             r = op.cg(b, x, maxit=-n, dirichlet=dirichlet, resume=True)
-            row = {"config": name, "form": (["WP", "EL", "EL-iso", "WP-glob", "WP-pair"][form if storage == 0 else storage + 1]
+            row = {"config": name, "form": (["WP", "EL", "EL-iso", "WP-glob"][form if storage == 0 else storage + 1]
                              if storage not in (4, 5) else (["WP-qp", "EL-qp"][form] if storage == 4 else "WP-sym")),
                    "d": c.d, "N": c.N, "p": c.p, "flops_per_elem": oi["flops_per_elem"],
                    "fp64_TFs": oi["flops_per_elem"] * c.n_elem / t_apply / 1e12,
