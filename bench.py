@@ -304,12 +304,12 @@ SECONDARY = [("C1", "full"), ("C2p1", "full"), ("C2p2", "full"), ("C2p3", "full"
 STORE_CODE = {"full": 0, "iso": 1, "global": 2, "sym": 5}
 
 
-def alg_bytes(oinfo: dict, n_elem: int, ndof: int) -> int:
+def alg_bytes(oinfo: dict, n_elem: int, ndof: int, n_wlattice: int = 0) -> int:
     """Algorithmic bytes of one apply: streamed weights of real elements
-    + u read once + y written once (GLOBAL: the W-lattice vector read once)."""
+    + u read once + y written once (GLOBAL: the W-lattice values read once)."""
     st = oinfo["storage"]
     if st == 2:
-        return int(oinfo["weight_bytes"]) + 16 * ndof
+        return 8 * n_wlattice + 16 * ndof
     n_w = oinfo["W_T"] + oinfo["n_c"] if st == 1 else oinfo["W_T"] * oinfo["n_c"]
     return 8 * n_w * n_elem + 16 * ndof
 
@@ -391,7 +391,7 @@ def secondary_configs(args, stream) -> list:
         op.cg(b, x, rtol=0.0, maxit=K, dirichlet=dirichlet, resume=True)     # builds the CG graph
         r = op.cg(b, x, rtol=0.0, maxit=K, dirichlet=dirichlet, resume=True)  # K iterations, one graph
         clk = sampler.stop()
-        ab = alg_bytes(oi, c.n_elem, c.ndof)
+        ab = alg_bytes(oi, c.n_elem, c.ndof, (2 * c.p * c.N + 1) ** c.d)
         fl = oi["flops_per_elem"] * c.n_elem
         t_burst = float(np.min(tb))
         rows.append({"config": name, "storage": storage, "form": "EL" if form == 1 else "WP", "d": c.d, "N": c.N,
@@ -479,7 +479,9 @@ def run_product(args, cfg) -> None:
 
     # algorithmic bytes of one apply on this rank: streamed weights of
     # real elements + u read once + y written once
-    alg_b = alg_bytes(oinfo, info["n_elem_local"], info["ndof_local"])
+    L = info["z1"] - info["z0"]
+    alg_b = alg_bytes(oinfo, info["n_elem_local"], info["ndof_local"],
+                      (2 * cfg.p * cfg.N + 1) ** (cfg.d - 1) * (2 * cfg.p * L + 1))
     flops_apply = oinfo["flops_per_elem"] * info["n_elem_local"]
     peak, peak_src = _measured_peaks()
     achieved = alg_b / t_apply / 1e9

@@ -82,9 +82,11 @@ extern "C" {
                                 stores W_T + d(d+1)/2 doubles per element instead of W_T d(d+1)/2 */
 #define DOGIP_STORE_GLOBAL 2 /* WP only (Theorem 1): one global diagonal over the
                                 double-grid space W = C_{N,2p}, A_ii = int_Omega m phi^W_i, stored
-                                as a W-lattice vector ((2pN+1)^d doubles) holding A_ii / mult_i
+                                as a W-lattice vector ((2pN+1)^d values) holding A_ii / mult_i
                                 (mult_i = elements sharing W node i, each visits it once) and
-                                gathered per element; multi-rank needs the NCCL communicator */
+                                gathered per element; kept class-major along x (x = 2p c + k at
+                                k (N+1) + c: rows of 2p(N+1) doubles) so a tile's lanes gather
+                                consecutive values; multi-rank needs a communicator */
 #define DOGIP_STORE_SYM    5 /* WP only: the same weights in symmetry-adapted form -- per orbit P of
                                 the double-grid nodes under the barycentric involutions
                                 G = <(0 1), (2 3)> (3D) / <(0 1)> (2D), ahat_psi(P) = (1/|G|) sum_g

@@ -122,7 +122,7 @@ def main():
             nw = oi["W_T"] + oi["n_c"] if storage == 1 else oi["W_T"] * oi["n_c"]
             alg = 8 * nw * c.n_elem + 16 * c.ndof
             if storage == 2:                      # global W vector read once (Theorem 1)
-                alg = oi["weight_bytes"] + 16 * c.ndof
+                alg = 8 * (2 * c.p * c.N + 1) ** c.d + 16 * c.ndof
             if storage == 4:                      # comparator: no stored operator data
                 alg = 16 * c.ndof
             b = op.load_vector(1.0, dirichlet=dirichlet)

@@ -361,7 +361,8 @@ def test_global_wp_storage_theorem1(d, N, p):
     verts = jitter_verts(d, N)
     m = Mesh(d, N, p, verts)
     op = Operator(m, 0, coef, storage=2)
-    assert op.info["weight_bytes"] == 8 * (2 * p * N + 1) ** d
+    # one W-lattice vector, stored class-major along x: rows of 2p (N + 1) doubles
+    assert op.info["weight_bytes"] == 8 * 2 * p * (N + 1) * (2 * p * N + 1) ** (d - 1)
     ed = oa.build(d, N, p, verts)
     A = oa.assemble_csr(ed, 0, coef)
     u = u_vector(ed.ndof, 0)
