@@ -236,15 +236,33 @@ __device__ __forceinline__ void lockstep_tail(int64_t gw, int64_t tile_end, int6
 // double-grid node j of the element is gathered from the global W-lattice vector, stored
 // class-major along x (x = 2p c + k at k (Nx+1) + c), so a tile's 32 lanes read 32
 // consecutive doubles per node; offw holds each node's offset in that layout.
+#ifndef DOGIP_GLOB_AHEAD
+#define DOGIP_GLOB_AHEAD 8     // W values loaded this many nodes ahead into registers (0 = on demand;
+                               // C5 GLOBAL 2.275 -> 2.214 ms, profiles/r02_ab_global_ahead.log)
+#endif
+template <int WT>
 struct GatherPol {
+    static constexpr int D = DOGIP_GLOB_AHEAD;
     const double* wg;      // global W weights of this slab
     const int* offw;       // shared-memory W-lattice offsets of this simplex type
     int64_t baseW;         // W-lattice index of the cell origin
+    double buf[D > 0 ? D : 1];   // node k's value sits in buf[k % D] (registers: k is a literal)
+    __device__ __forceinline__ double ld(int k) const { return __ldg(wg + baseW + offw[k]); }
     template <int J>
-    __device__ __forceinline__ void begin() {}
+    __device__ __forceinline__ void begin() {
+        if constexpr (J == 0 && D > 0) {
+#pragma unroll
+            for (int k = 0; k < D && k < WT; ++k) buf[k] = ld(k);
+        }
+    }
     template <int J>
     __device__ __forceinline__ void end() {}
-    __device__ __forceinline__ double w(int k) const { return __ldg(wg + baseW + offw[k]); }
+    __device__ __forceinline__ double w(int k) {
+        if constexpr (D == 0) return ld(k);
+        const double v = buf[k % D];
+        if (k + D < WT) buf[k % D] = ld(k + D);   // the load runs while node k is computed
+        return v;
+    }
 };
 
 // Per-tile gather context of one lane's element.
@@ -443,7 +461,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
 #pragma unroll
         for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
         if constexpr (GLOB) {
-            GatherPol gp{w, offw_s + cur.s * MAX_WT_GLOBAL,
+            GatherPol<RE::WT> gp{w, offw_s + cur.s * MAX_WT_GLOBAL,
                          geo.rw * (int64_t)(2 * geo.p) * (cur.cj + geo.swy * cur.ck) + cur.ci};
             RE::body(uT, yT, gp);
         } else {
