@@ -993,3 +993,50 @@ def test_element_kernel_path_for_small_p():
     assert r.returncode == 0, r.stderr[-2000:]
     worst = float([l for l in r.stdout.splitlines() if l.startswith("WORST")][0].split()[1])
     assert worst <= TOL, worst
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(12))
+def test_randomised_configurations(seed):
+    """Seeded random draws over (d, N, p, form, storage, coefficient, jitter, Dirichlet,
+    slab split): apply against the assembled oracle A, and for several slabs the partial
+    sums against the single-rank apply -- a net over combinations the targeted tests do not
+    enumerate (ragged x-blocks, N from 1 to 40, every storage the form admits)."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([2, 3]))
+    p = int(rng.integers(1, 5))
+    N = int(rng.integers(1, 41 if d == 2 else (9 if p <= 2 else 5)))
+    form = int(rng.integers(0, 2))
+    stores = [0, 2, 4, 5] if form == 0 else [0, 1, 4]
+    store = int(rng.choice(stores))
+    jit = bool(rng.integers(0, 2)) and N >= 2
+    verts = jitter_verts(d, N, seed=int(rng.integers(0, 100))) if jit else None
+    if form == 0:
+        coef = coef_for(d, 0, "tanh") if rng.integers(0, 2) else Coefficient(COEF_CONST, np.array([0.7]))
+    elif store == 1:
+        coef = Coefficient(COEF_PER_CELL, np.zeros(0), grf_per_cell(d, N, 0.2, 1.0, int(rng.integers(0, 50))))
+    else:
+        coef = ANISO if (d == 3 and rng.integers(0, 2)) else Coefficient(COEF_PER_CELL, np.zeros(0),
+                                                                         grf_per_cell(d, N, 0.2, 1.0, 7))
+    dirichlet = bool(rng.integers(0, 2))
+    ed = oa.build(d, N, p, verts)
+    A = oa.assemble_csr(ed, form, coef)
+    ref_op = oa.dirichlet_matrix(A, boundary_mask(d, N, p)) if dirichlet else A
+    u = u_vector(ed.ndof, seed)
+    m = Mesh(d, N, p, verts, device=0)
+    op = Operator(m, form, coef, storage=store)
+    y = op.apply(torch.from_numpy(u).cuda(), dirichlet=dirichlet).cpu().numpy()
+    case = (d, N, p, form, store, coef.kind, jit, dirichlet)
+    assert relerr(y, ref_op @ u) <= TOL, case
+    nr = int(rng.integers(2, 4))
+    if N >= nr and store != 2 and not dirichlet:        # partial sums of a slab split
+        acc = np.zeros_like(u)
+        for r in range(nr):
+            ms = Mesh(d, N, p, verts, rank=r, nranks=nr, device=0)
+            ops = Operator(ms, form, coef, storage=store)
+            i0 = ms.info["dof_offset"]
+            acc[i0:i0 + ms.ndof] += ops.apply(torch.from_numpy(u[i0:i0 + ms.ndof].copy()).cuda(),
+                                              exchange=False).cpu().numpy()
+        assert relerr(acc, A @ u) <= 1e-13, case + (nr,)
