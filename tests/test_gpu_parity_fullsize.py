@@ -56,7 +56,7 @@ def _rows_near_faces(d, N, p, rng, n_rand=40):
     return np.unique(np.array(rows, dtype=np.int64))
 
 
-@pytest.mark.parametrize("name", ["C3", "C4", "C2p3"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C2p1", "C2p2", "C2p3", "C2p4"])
 def test_full_size_dirichlet_sampled_rows(name):
     torch = _torch()
     from paper_1710_09913_b200.api import Mesh, Operator
