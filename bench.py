@@ -19,8 +19,20 @@ CG iterations; ms_per_step = device time of one CG iteration (max over ranks).
 Inputs (21 GB of weights per GPU at N=1) are far larger than the 126 MB L2,
 so no L2 flush is needed between iterations.
 
---impl reference: the CPU oracle (oracle/, plain NumPy) timed on a bounded
-sample of the same workload on the host cores (rank 0 only).
+Launch: --gpus N without torchrun starts N ranks itself (torch.distributed.run on
+127.0.0.1, one process per GPU, NCCL) and fails clearly when fewer than N GPUs are
+visible; under torchrun WORLD_SIZE must equal --gpus.
+
+Also on the line (rank 0): e2e (dogip_apply_host: pinned host u in, y out, copies inside
+the timed region), e2e_cg (dogip_cg one iteration per call with the residual read back),
+roofline (algorithmic bytes / event time / measured copy bandwidth; traffic from the
+committed ncu capture), clocks sampled during the timed region, gpu_launches, and at
+N = 1 the `configs` block (every BASELINE.json config and storage, each apply a CUDA-graph
+replay with the L2 flushed before it, plus a burst number and the clocks seen) and
+cpu_baseline (the oracle on all host cores, in a separate process).
+
+--impl reference: the CPU oracle (oracle/, plain NumPy, one worker process per host core)
+timed on a bounded sample of the same workload (rank 0 only).
 """
 from __future__ import annotations
 
