@@ -756,10 +756,13 @@ static QpArgs qp_args(dogip_op op, const ApplyArgs& a) {
 
 // y = A u (+ exchange); with dot != null also *dot = u^T y over this rank's elements
 // (+ boundary rows owned by this rank), fused into the apply kernel (CG's p.q).
+constexpr int MAX_APPLY_LAUNCHES = 3;   // per apply: boundary layers (2) + interior
+
 static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, cudaStream_t st,
                       double* dot = nullptr, const double* skip_if = nullptr) {
     dogip_mesh_s* m = op->m;
     const SlabGeo& g = m->geo;
+    const bool xchg = m->comm && !(flags & DOGIP_NO_EXCHANGE);
     CK(cudaMemsetAsync(y, 0, sizeof(double) * g.ndof, st));
     ApplyArgs a{};
     a.d = m->d; a.p = m->p; a.form = op->form; a.store = op->store;
@@ -771,22 +774,23 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
     a.skip_if = skip_if;
     bool rows_written = false;
     a.rows_written = &rows_written;
-    int nslots[3] = {0, 0, 0};
+    int nslots[MAX_APPLY_LAUNCHES] = {};
     int nl = 0;
     if (dot && !op->dotp) {
-        CK(cudaMalloc(&op->dotp, sizeof(double) * 3 * APPLY_MAX_WARPS));
+        CK(cudaMalloc(&op->dotp, sizeof(double) * MAX_APPLY_LAUNCHES * APPLY_MAX_WARPS));
         CK(cudaMalloc(&op->bpart, sizeof(double) * RED_BLOCKS));
     }
+    int64_t slot0 = 0;   // the launches' per-warp partials of p.q are packed back to back
     auto launch = [&](int64_t t0, int64_t t1) -> cudaError_t {
         a.tile_begin = t0;
         a.tile_end = t1;
-        a.dot_partials = dot ? op->dotp + (size_t)nl * APPLY_MAX_WARPS : nullptr;
+        a.dot_partials = dot ? op->dotp + slot0 : nullptr;
         a.dot_nslots = &nslots[nl];
+        const cudaError_t e = op->store == DOGIP_STORE_QP ? launch_qp_apply(qp_args(op, a)) : launch_apply(a);
+        slot0 += nslots[nl];
         ++nl;
-        if (op->store == DOGIP_STORE_QP) return launch_qp_apply(qp_args(op, a));
-        return launch_apply(a);
+        return e;
     };
-    const bool xchg = m->comm && !(flags & DOGIP_NO_EXCHANGE);
     if (!xchg) {
         CK(launch(0, g.ntiles));
     } else {
@@ -807,8 +811,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
         RET(finish_exchange(m, y, st));
     }
     if (dot) {
-        for (int i = 0; i < nl; ++i)
-            CK(launch_sum_partials(op->dotp + (size_t)i * APPLY_MAX_WARPS, nslots[i], i ? dot : nullptr, dot, st));
+        CK(launch_sum_partials(op->dotp, (int)slot0, nullptr, dot, st));
     }
     // the cell-per-lane kernel (p <= 2) writes the Dirichlet rows itself (one owner per row,
     // its u_i^2 in the fused dot); the other kernels take the separate fix-up
@@ -1065,7 +1068,7 @@ extern "C" int dogip_cg(dogip_op op, const double* b, double* x, double rtol, in
         CK(cudaMallocHost(&op->h_scal, sizeof(double) * S_COUNT));
     }
     if (!op->dotp) {
-        CK(cudaMalloc(&op->dotp, sizeof(double) * 3 * APPLY_MAX_WARPS));
+        CK(cudaMalloc(&op->dotp, sizeof(double) * MAX_APPLY_LAUNCHES * APPLY_MAX_WARPS));
         CK(cudaMalloc(&op->bpart, sizeof(double) * RED_BLOCKS));
     }
     const unsigned aflags = flags & DOGIP_DIRICHLET_ZERO;
