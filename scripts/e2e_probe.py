@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Host-buffer apply (C4) vs raw pinned-copy bandwidth: is the pipelined e2e copy-bound?
 
-    python scripts/e2e_probe.py            # DOGIP_HOST_CHUNKS sweeps 4..64 via env in a loop
+    python scripts/e2e_probe.py            # DOGIP_HOST_CHUNKS sweep via env
 """
 import json
 import os
@@ -50,8 +50,9 @@ m = Mesh(c.d, c.N, c.p, c.vertices())
 op = Operator(m, c.forms[0], c.coefficient())
 u = torch.from_numpy(c.u()).pin_memory()
 y = torch.empty_like(u).pin_memory()
-for k in (4, 8, 16, 32, 64):
+for k in (8, 16, 24, 32):
     os.environ["DOGIP_HOST_CHUNKS"] = str(k)
     out[f"apply_host_ms_K{k}"] = timed(lambda: op.apply_host_ptr(u.data_ptr(), y.data_ptr(), dirichlet=c.forms[0] == 1))
+os.environ.pop("DOGIP_HOST_CHUNKS")
 out["apply_device_ms"] = timed(lambda: op.apply(d1, d2, dirichlet=c.forms[0] == 1))
 print(json.dumps(out))
