@@ -343,6 +343,102 @@ __device__ __forceinline__ void scatter(double* __restrict__ y, const ElemCtx& c
     }
 }
 
+
+// Pair combine (round 2).  The 4 warps of a CTA hold consecutive tiles, and tiles are
+// ordered with the simplex type s fastest, so warps 2i and 2i+1 always hold types (2m, 2m+1)
+// of the SAME 32 cells (tile ranges start and end on whole cell rows).  Those two simplices
+// share a face (3D Kuhn types 0|1, 2|3, 4|5 differ by one adjacent transposition; 2D: the
+// diagonal edge), so the even warp hands its y_T values on the shared DoFs to the odd warp
+// through shared memory (one 64-thread named barrier per tile, double-buffered) and skips
+// their atomics: 3D P4 70 -> 55, 3D P3 40 -> 30 red.global.add.f64 per element pair.
+#ifndef DOGIP_PAIR_COMBINE
+#define DOGIP_PAIR_COMBINE 1
+#endif
+template <class RE>
+__host__ __device__ constexpr int loff_dim() { return (int)(sizeof(RE::LOFF[0][0]) / sizeof(RE::LOFF[0][0][0])); }
+// local DoF of simplex s0 + 1 at the same lattice point as DoF l0 of simplex s0 (-1: none)
+template <class RE>
+__host__ __device__ constexpr int pair_partner(int s0, int l0) {
+    for (int l = 0; l < RE::VT; ++l) {
+        bool eq = true;
+        for (int a = 0; a < loff_dim<RE>(); ++a)
+            if (RE::LOFF[s0][l0][a] != RE::LOFF[s0 + 1][l][a]) eq = false;
+        if (eq) return l;
+    }
+    return -1;
+}
+template <class RE>
+__host__ __device__ constexpr int pair_slot(int s0, int l0) {   // index among the shared DoFs
+    int k = 0;
+    for (int l = 0; l < l0; ++l) k += pair_partner<RE>(s0, l) >= 0;
+    return k;
+}
+template <class RE>
+__host__ __device__ constexpr int pair_shared_max() {
+    int m = 0;
+    for (int s0 = 0; s0 + 1 < RE::NS; s0 += 2) {
+        const int k = pair_slot<RE>(s0, RE::VT);
+        m = k > m ? k : m;
+    }
+    return m;
+}
+template <class RE>
+__host__ __device__ constexpr uint64_t pair_mask(int s0) {
+    uint64_t m = 0;
+    for (int l = 0; l < RE::VT; ++l)
+        if (pair_partner<RE>(s0, l) >= 0) m |= 1ull << l;
+    return m;
+}
+template <class RE, int S0, int L = 0>
+__device__ __forceinline__ void pair_put(const double* yT, double* buf) {
+    if constexpr (L < RE::VT) {
+        if constexpr (pair_partner<RE>(S0, L) >= 0) buf[pair_slot<RE>(S0, L) * TILE] = yT[L];
+        pair_put<RE, S0, L + 1>(yT, buf);
+    }
+}
+template <class RE, int S0, int L = 0>
+__device__ __forceinline__ void pair_get(double* yT, const double* buf) {
+    if constexpr (L < RE::VT) {
+        constexpr int l1 = pair_partner<RE>(S0, L);
+        if constexpr (l1 >= 0) yT[l1] += buf[pair_slot<RE>(S0, L) * TILE];
+        pair_get<RE, S0, L + 1>(yT, buf);
+    }
+}
+// put (even warp): returns the mask of the DoFs handed over; get (odd warp): 0
+template <class RE, int S0 = 0>
+__device__ __forceinline__ uint64_t pair_dispatch(bool put, int ps, double* yT, double* buf) {
+    if constexpr (S0 + 1 < RE::NS) {
+        if (ps == S0 / 2) {
+            constexpr uint64_t mask = pair_mask<RE>(S0);
+            if (put) { pair_put<RE, S0>(yT, buf); return mask; }
+            pair_get<RE, S0>(yT, buf);
+            return 0;
+        }
+        return pair_dispatch<RE, S0 + 2>(put, ps, yT, buf);
+    }
+    return 0;
+}
+// Before the scatter of a tile of type s (warp-uniform): returns the DoFs this warp must not
+// scatter (the even warp's shared DoFs).  buf = this pair's [2][F][32] buffer, par = tile parity.
+template <class RE>
+__device__ __forceinline__ uint64_t pair_combine(double* yT, double* buf, int par, int s, int warp, int lane) {
+    constexpr int F = pair_shared_max<RE>();
+    double* b = buf + (size_t)par * F * TILE + lane;
+    const bool even = (s & 1) == 0;
+    uint64_t m = 0;
+    if (even) m = pair_dispatch<RE>(true, s >> 1, yT, b);
+    asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp >> 1)) : "memory");
+    if (!even) pair_dispatch<RE>(false, s >> 1, yT, b);
+    return m;
+}
+// On for the 3D elliptic kernels (C4 full 3.56 -> 3.53 ms, iso 2.16 -> 2.10); off for WP
+// (C5 sym / full / global neutral to +1 %) and 2D (C2 p=4 iso +11 %):
+// profiles/r02_ab_pair_combine.log
+template <class RE, int D, int F>
+__host__ __device__ constexpr bool pair_enabled() {
+    return DOGIP_PAIR_COMBINE && D == 3 && F == 1 && !direct_weights<RE>() && APPLY_THREADS % 64 == 0;
+}
+
 template <int D, int P, int F, int ST, bool DIR, bool GLOB>
 __global__ void __launch_bounds__(APPLY_THREADS, min_blocks<dogip_gen::RefElem<D, P, F, ST>>())
 apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
@@ -359,6 +455,11 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (RING ? (size_t)NW * C::S * C::ROWS * TILE : 0));
     constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
     double* ubufs = reinterpret_cast<double*>(bars + (RING ? NW * C::S : 0));   // [NW][VT][32] (UPF only)
+    constexpr bool PAIRC = pair_enabled<RE, D, F>();
+    constexpr int PF = pair_shared_max<RE>();
+    double* pbuf = !PAIRC ? nullptr : ubufs + (UPF ? (size_t)NW * RE::VT * TILE : 0) +
+                   (size_t)((threadIdx.x >> 5) >> 1) * 2 * PF * TILE;      // [NW/2][2][PF][32]
+    int ppar = 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw = tile_begin + (int64_t)blockIdx.x * NW + warp;
@@ -448,7 +549,9 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
             for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
             if constexpr (RE::DOT_IN_BODY) RE::body(uT, yT, ws, dot_partials ? &udot : nullptr);
             ws.next_tile();
-            if (prev.valid) scatter<RE>(y, prev, yT);
+            ElemCtx sc = prev;
+            if constexpr (PAIRC) { sc.skip |= pair_combine<RE>(yT, pbuf, ppar, prev.s, warp, lane); ppar ^= 1; }
+            if (sc.valid) scatter<RE>(y, sc, yT);
         }
         lockstep_tail<RE, C>(gw, tile_end, tile_begin + (int64_t)blockIdx.x * NW, nw);
     } else {
@@ -475,7 +578,8 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
 #pragma unroll
             for (int l = 0; l < RE::VT; ++l) udot = fma(uT[l], yT[l], udot);
         }
-        const ElemCtx prev = cur;
+        ElemCtx prev = cur;
+        if constexpr (PAIRC) { prev.skip |= pair_combine<RE>(yT, pbuf, ppar, prev.s, warp, lane); ppar ^= 1; }
         if (tile + nw < tile_end) {            // next tile's gather overlaps this scatter
             cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
             gather<RE>(u, cur, uT);
@@ -498,7 +602,8 @@ cudaError_t launch_one(const ApplyArgs& a) {
     constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
     constexpr bool DW = direct_weights<RE>() && !GLOB;
     const size_t smem = ((GLOB || DW) ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8) +
-                        (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0);
+                        (UPF ? (size_t)NW * RE::VT * TILE * 8 : 0) +
+                        (pair_enabled<RE, D, F>() ? (size_t)(NW / 2) * 2 * pair_shared_max<RE>() * TILE * 8 : 0);
     auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
     static std::atomic<uint64_t> cfg[MAX_DEVICES];   // per instantiation, per device
     int occ = 1;
