@@ -564,8 +564,10 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
 #pragma unroll
         for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
         if constexpr (GLOB) {
+            // padding lanes (ci >= Nx) gather the slab's first cell: in bounds and finite
+            // (their u_T is 0, so y_T = 0 and the fused p.q stays exact)
             GatherPol<RE::WT> gp{w, offw_s + cur.s * MAX_WT_GLOBAL,
-                         geo.rw * (int64_t)(2 * geo.p) * (cur.cj + geo.swy * cur.ck) + cur.ci};
+                         cur.valid ? geo.rw * (int64_t)(2 * geo.p) * (cur.cj + geo.swy * cur.ck) + cur.ci : 0};
             RE::body(uT, yT, gp);
         } else {
             if constexpr (RE::DOT_IN_BODY) RE::body(uT, yT, ws, dot_partials ? &udot : nullptr);
