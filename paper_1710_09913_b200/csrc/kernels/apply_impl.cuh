@@ -237,8 +237,9 @@ __device__ __forceinline__ void lockstep_tail(int64_t gw, int64_t tile_end, int6
 // class-major along x (x = 2p c + k at k (Nx+1) + c), so a tile's 32 lanes read 32
 // consecutive doubles per node; offw holds each node's offset in that layout.
 #ifndef DOGIP_GLOB_AHEAD
-#define DOGIP_GLOB_AHEAD 8     // W values loaded this many nodes ahead into registers (0 = on demand;
-                               // C5 GLOBAL 2.275 -> 2.214 ms, profiles/r02_ab_global_ahead.log)
+#define DOGIP_GLOB_AHEAD 4     // W values loaded this many nodes ahead into registers (0 = on demand;
+                               // C5 GLOBAL 2.275 -> 2.214 ms at 8, profiles/r02_ab_global_ahead.log;
+                               // 2.265 -> 2.195 ms at 4 on the final build, r02_ab_global_ahead_final.log)
 #endif
 template <int WT>
 struct GatherPol {
