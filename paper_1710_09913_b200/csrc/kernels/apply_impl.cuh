@@ -26,6 +26,9 @@
 //    scattered with fire-and-forget red.global.add.f64 (y zeroed first), so the
 //    gather latency overlaps the scatter; DIRICHLET zeroes boundary DoFs of u_T
 //    and skips their scatter (the boundary rows are fixed by dirichlet_fixup).
+//  * 3D EL: warps 2i / 2i+1 hold Kuhn types 2m / 2m+1 of the same cells, which share a
+//    face; the even warp hands its y_T on that face to the odd one through shared memory
+//    before the scatter (pair combine, 25 % fewer atomics).
 // Kernels in this file:
 //  * apply_kernel       element per lane (above): p >= 3 (2D p = 4), ISO, SYM, GLOBAL;
 //  * apply_cell_kernel  cell per lane (all d! simplices of a cell, DoFs shared on chip,
