@@ -135,3 +135,40 @@ def test_negative_control_weight_perturbation(d, N, p, form):
     assert err() > 1e3 * TOL
     op._test_perturb_weight(e, j, 0, -delta)
     assert err() <= TOL
+
+
+@pytest.mark.parametrize("storage,dirichlet", [(0, True), (0, False), (1, True), (1, False)])
+def test_ragged_xblocks_3d_el_element_kernel(storage, dirichlet):
+    """The C4 recipe at N = 37: two x-blocks per cell row (32 + a ragged 5), the 3D P3 EL
+    element kernel with its even/odd-warp pair combine of the shared Kuhn faces, FULL and
+    ISO storage, with and without Dirichlet elimination; sampled rows near every face
+    (incl. the last valid lane of the ragged block) against the oracle."""
+    torch = _torch()
+    from paper_1710_09913_b200.api import Mesh, Operator
+    c = get_config("C4").with_size(37)
+    coef, verts, form = c.coefficient(), c.vertices(), c.forms[0]
+    m = Mesh(c.d, c.N, c.p, verts)
+    op = Operator(m, form, coef, storage=storage)
+    u = c.u()
+    y = op.apply(torch.from_numpy(u).cuda(), dirichlet=dirichlet).cpu().numpy()
+    M = c.p * c.N + 1
+    rng = np.random.default_rng(37 + storage)
+    rows = _rows_near_faces(c.d, c.N, c.p, rng)
+    # plus the DoFs of the cells at the x-block seam (cells 31 | 32) and of the last cell
+    extra = []
+    for X in (3 * 31, 3 * 32, 3 * 32 + 1, 3 * 36, 3 * 37 - 1):
+        for _ in range(4):
+            lat = rng.integers(1, M - 1, 3)
+            lat[0] = X
+            extra.append(int(lat[0] + M * lat[1] + M * M * lat[2]))
+    rows = np.unique(np.concatenate([rows, np.array(extra, dtype=np.int64)]))
+    scale = np.abs(y).max()
+    if dirichlet:
+        lat = np.stack([(rows // M ** a) % M for a in range(3)], axis=1)
+        bnd = np.any((lat == 0) | (lat == M - 1), axis=1)
+        assert np.array_equal(y[rows[bnd]], u[rows[bnd]])
+        rows = rows[~bnd]
+        ref = oa.apply_rows_sampled(c.d, c.N, c.p, verts, form, coef, _boundary_zeroed(u, 3, M), rows)
+    else:
+        ref = oa.apply_rows_sampled(c.d, c.N, c.p, verts, form, coef, u, rows)
+    assert np.abs(y[rows] - ref).max() / scale <= TOL
