@@ -79,6 +79,7 @@ struct dogip_mesh_s {
 struct dogip_op_s {
     dogip_mesh_s* m = nullptr;
     int form = 0, nq = 0, store = 0;
+    int kstore = 0;           // storage the apply kernels are instantiated for (6: FULL WP, symmetry-adapted body)
     RefInfo ref{};
     double* d_w = nullptr;
     int64_t w_doubles = 0;
@@ -490,7 +491,11 @@ extern "C" int dogip_weights_ex(dogip_mesh m, int form, const dogip_coeff* coeff
     op->m = m;
     op->form = form;
     op->store = storage;
-    ref_info(d, p, form, (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_QP) ? 0 : storage, op->ref);
+    op->kstore = storage;
+    // FULL weighted projection: the same a_{T,j} with rows in orbit order where the
+    // symmetry-adapted body is instantiated (internal kernel storage 6)
+    if (storage == DOGIP_STORE_FULL && form == DOGIP_WP && ref_info(d, p, form, 6, op->ref)) op->kstore = 6;
+    else ref_info(d, p, form, (storage == DOGIP_STORE_GLOBAL || storage == DOGIP_STORE_QP) ? 0 : storage, op->ref);
     const int WT = op->ref.WT, NC = op->ref.NC, VT = op->ref.VT;
     const int n1d = quad_n1d > 0 ? quad_n1d : p + 3;
     std::vector<double> pts, wts;
@@ -765,7 +770,7 @@ static int apply_impl(dogip_op op, const double* u, double* y, unsigned flags, c
     const bool xchg = m->comm && !(flags & DOGIP_NO_EXCHANGE);
     CK(cudaMemsetAsync(y, 0, sizeof(double) * g.ndof, st));
     ApplyArgs a{};
-    a.d = m->d; a.p = m->p; a.form = op->form; a.store = op->store;
+    a.d = m->d; a.p = m->p; a.form = op->form; a.store = op->kstore;
     a.offw = op->d_offw;
     a.dirichlet = (flags & DOGIP_DIRICHLET_ZERO) != 0;
     a.u = u; a.y = y; a.w = op->d_w; a.geo = g; a.tab = &m->tab;
@@ -884,7 +889,7 @@ static int apply_host_pipelined(dogip_op op, const double* u_host, double* y_hos
         CK(cudaEventRecord(op->ev_in[c], op->s_h2d));
         CK(cudaStreamWaitEvent(st, op->ev_in[c], 0));
         ApplyArgs aa{};
-        aa.d = m->d; aa.p = p; aa.form = op->form; aa.store = op->store;
+        aa.d = m->d; aa.p = p; aa.form = op->form; aa.store = op->kstore;
         aa.offw = op->d_offw;
         aa.dirichlet = dir;
         aa.u = op->hu; aa.y = op->hy; aa.w = op->d_w; aa.geo = g; aa.tab = &m->tab;
@@ -1324,7 +1329,7 @@ extern "C" int dogip_export_weights(dogip_op op, double* host, int64_t cap) {
             for (int j = 0; j < WT; ++j)
                 for (int c = 0; c < NC; ++c)
                     host[(e * WT + j) * NC + c] =
-                        op->store == DOGIP_STORE_ISO ? at(op->ref.NG + op->ref.rowperm[j]) * at(c) : at(j * NC + c);
+                        op->store == DOGIP_STORE_ISO ? at(op->ref.NG + op->ref.rowperm[j]) * at(c) : at(op->ref.rowperm[j] * NC + c);
         }
     return DOGIP_OK;
 }
@@ -1343,7 +1348,7 @@ extern "C" int dogip_test_perturb_weight(dogip_op op, int64_t elem, int j, int c
     const int64_t s = elem % g.ns, cell = elem / g.ns;
     const int64_t ci = cell % g.Nx, cj = (cell / g.Nx) % g.Ny, ck = cell / ((int64_t)g.Nx * g.Ny);
     const int64_t tile = s + g.ns * (ci / TILE + g.nxb * (cj + (int64_t)g.Ny * ck));
-    const size_t idx = ((size_t)tile * op->ref.tile_rows + (size_t)(j * NC + c)) * TILE + (size_t)(ci % TILE);
+    const size_t idx = ((size_t)tile * op->ref.tile_rows + (size_t)(op->ref.rowperm[j] * NC + c)) * TILE + (size_t)(ci % TILE);
     DeviceGuard dg(op->m->device);
     double v = 0.0;
     CK(cudaMemcpy(&v, op->d_w + idx, sizeof(double), cudaMemcpyDeviceToHost));

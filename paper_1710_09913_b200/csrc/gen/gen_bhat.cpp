@@ -283,7 +283,11 @@ static void emit_variant(FILE* f, int d, int p, int form, int store) {
 // instead of 1729, ~2240 instead of ~3340 FP64 instructions per element.
 // Emitted body: v = adapted u (butterflies), per W orbit: ghat (block rows), hhat =
 // weight matrix x ghat, z += Btilde^T hhat; y = inverse butterflies of z / |G|.
-static void emit_sym(FILE* f, int d, int p) {
+// raw = true (STORE 6, internal): the plain element-wise weights a_{T,j} of
+// DOGIP_STORE_FULL, rows permuted into the same orbit order (ROWPERM), and the body forms
+// ahat_psi(P) = (1/s) sum_c psi(c) a_{c j0} from the orbit's s raw values (butterflies)
+// before the weight multiply: FULL storage through the symmetry-adapted body.
+static void emit_sym(FILE* f, int d, int p, bool raw = false) {
     Table t = bhat_table(d, p, 0);
     const int VT = t.cols, WT = t.rows;
     auto A = multi_indices(d, p);
@@ -388,9 +392,9 @@ static void emit_sym(FILE* f, int d, int p) {
     int nnz = 0, pm1 = 0;
     for (auto& v : t.v) { nnz += !v.is_zero(); pm1 += v.is_pm1(); }
     auto simp = cell_simplices(d);
-    std::fprintf(f, "template <> struct RefElem<%d, %d, 0, 5> {\n", d, p);
-    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 1, HAS_ROWPERM = 0;\n",
-                 VT, WT, WT, (int)simp.size(), NGR);
+    std::fprintf(f, "template <> struct RefElem<%d, %d, 0, %d> {\n", d, p, raw ? 6 : 5);
+    std::fprintf(f, "    static constexpr int VT = %d, WT = %d, NC = 1, NG = 0, ROWS = 12, TILE_ROWS = %d, NS = %d, RALIGN = %d, PAIR = 0, DOT_IN_BODY = 1, HAS_ROWPERM = %d;\n",
+                 VT, WT, WT, (int)simp.size(), NGR, raw ? 1 : 0);
     std::fprintf(f, "    static constexpr int NNZ = %d, NNZ_PM1 = %d, NGROUP = %d;\n", nnz, pm1, NGR);
     std::fprintf(f, "    static constexpr signed char LOFF[%d][%d][%d] = {", (int)simp.size(), VT, d);
     for (size_t si = 0; si < simp.size(); ++si) {
@@ -411,7 +415,24 @@ static void emit_sym(FILE* f, int d, int p) {
     for (int l = 0; l < VT; ++l)
         std::fprintf(f, "%s{%d,%d,%d}", l ? "," : "", A[l][1], A[l][2], d == 3 ? A[l][3] : 0);
     std::fprintf(f, "};\n");
+    if (raw) {
+        // ROWPERM[j] = stored row of W node j: member k of orbit P (in the order of rj) at
+        // row wrow[P][0] + k
+        std::vector<int> perm(WT, -1);
+        for (size_t P = 0; P < OW.size(); ++P)
+            for (int k = 0; k < 4; ++k) {
+                const int j = rj[wrow[P][0]][k];
+                if (j >= 0) perm[j] = wrow[P][0] + k;
+            }
+        std::fprintf(f, "    static constexpr short ROWPERM[%d] = {", WT);
+        for (int j = 0; j < WT; ++j) {
+            if (perm[j] < 0) { std::fprintf(stderr, "sym raw: node without a row\n"); std::exit(1); }
+            std::fprintf(f, "%s%d", j ? "," : "", perm[j]);
+        }
+        std::fprintf(f, "};\n");
+    }
     // weights-kernel table: stored row r = sum_k SYMC[r][k] a_{SYMJ[r][k]}
+    if (!raw) {
     std::fprintf(f, "    static constexpr short SYMJ[%d][4] = {", WT);
     for (int r = 0; r < WT; ++r)
         std::fprintf(f, "%s{%d,%d,%d,%d}", r ? "," : "", rj[r][0], rj[r][1], rj[r][2], rj[r][3]);
@@ -421,6 +442,7 @@ static void emit_sym(FILE* f, int d, int p) {
         std::fprintf(f, "%s{%s,%s,%s,%s}", r ? "," : "", lit(rc[r][0].to_double()).c_str(), lit(rc[r][1].to_double()).c_str(),
                      lit(rc[r][2].to_double()).c_str(), lit(rc[r][3].to_double()).c_str());
     std::fprintf(f, "};\n");
+    }
     std::fprintf(f, "    static __host__ __device__ constexpr int row_of(int r) { return r; }\n");
     // dot != null: *dot += u_T . y_T, computed as v . z (Parseval over the characters:
     // sum_k v_k z_k = sum_l u_l y_l), so u_T dies after the transform (issuing the next
@@ -479,8 +501,33 @@ static void emit_sym(FILE* f, int d, int p) {
         const int j0 = PO.rep;
         std::fprintf(f, "        {\n          pol.template begin<%d>();\n", wrow[P][0]);
         // the orbit's weights first: their shared-memory latency overlaps the block rows
-        for (size_t q = 0; q < PO.chars.size(); ++q)
-            std::fprintf(f, "          const double a%zu = pol.w(%d);\n", q, wrow[P][q]);
+        if (!raw) {
+            for (size_t q = 0; q < PO.chars.size(); ++q)
+                std::fprintf(f, "          const double a%zu = pol.w(%d);\n", q, wrow[P][q]);
+        } else {
+            // raw a_{member k} at row wrow[P][0] + k; ahat_q = sum_k rc[q][k] r_k, rc = +-1/s
+            const int s = (int)PO.members.size();
+            for (int k = 0; k < s; ++k) std::fprintf(f, "          const double r%d = pol.w(%d);\n", k, wrow[P][0] + k);
+            auto sgn = [&](int q, int k) { return rc[wrow[P][q]][k].to_double() > 0 ? 1 : -1; };
+            if (s == 1) {
+                std::fprintf(f, "          const double a0 = r0;\n");
+            } else if (s == 2) {
+                for (int q = 0; q < 2; ++q)
+                    std::fprintf(f, "          const double a%d = (r0 %s r1) * 0.5;\n", q, sgn(q, 1) > 0 ? "+" : "-");
+                flops += 4;
+            } else {
+                // members k = 0..3 are e = 0..3 (distinct): ahat = ((r0 + s1 r1) + s2 (r2 + s1 r3)) / 4
+                for (int k = 0; k < 4; ++k)
+                    if (rj[wrow[P][0]][k] != gW[k][j0]) { std::fprintf(stderr, "sym raw: member order\n"); std::exit(1); }
+                std::fprintf(f, "          const double tp = r0 + r1, tm = r0 - r1, rp = r2 + r3, rm = r2 - r3;\n");
+                for (int q = 0; q < 4; ++q) {
+                    const bool s1 = sgn(q, 1) < 0, s2 = sgn(q, 2) < 0;
+                    if (sgn(q, 3) != (s1 == s2 ? 1 : -1)) { std::fprintf(stderr, "sym raw: character\n"); std::exit(1); }
+                    std::fprintf(f, "          const double a%d = (%s %s %s) * 0.25;\n", q, s1 ? "tm" : "tp", s2 ? "-" : "+", s1 ? "rm" : "rp");
+                }
+                flops += 12;
+            }
+        }
         // ghat_chi = sum_O Bhat_chi[P,O] uhat_chi(O), uhat = |H_O| v
         for (size_t ci = 0; ci < PO.chars.size(); ++ci) {
             const int ch = PO.chars[ci];
@@ -830,6 +877,7 @@ int main(int argc, char** argv) {
             if (g_iso_sym) emit_iso_sym(f, d, p);
             else emit_variant(f, d, p, 1, 1);
             emit_sym(f, d, p);
+            emit_sym(f, d, p, true);
         }
     std::fprintf(f, "}  // namespace dogip_gen\n");
     std::fclose(f);

@@ -11,6 +11,7 @@ bool ref_info_3_4(int form, int store, RefInfo& r) {
     if (form == 1 && store == 0) { fill_info<3, 4, 1, 0>(r); return true; }
     if (form == 1 && store == 1) { fill_info<3, 4, 1, 1>(r); return true; }
     if (form == 0 && store == 5) { fill_info<3, 4, 0, 5>(r); return true; }
+    if (full_sym_body<3, 4>() && form == 0 && store == 6) { fill_info<3, 4, 0, 6>(r); return true; }   // FULL, symmetry-adapted body
     return false;
 }
 

@@ -70,6 +70,10 @@
 #define DOGIP_ROWS_2CTA 24      // ... when 2 CTAs share an SM
 #endif
 
+#ifndef DOGIP_FULL_SYM
+#define DOGIP_FULL_SYM 1   // 0: FULL WP storage through the plain node-by-node body (A/B builds)
+#endif
+
 namespace dogip {
 
 namespace {
@@ -643,12 +647,21 @@ cudaError_t launch_dir(const ApplyArgs& a) {
     return a.dirichlet ? launch_one<D, P, F, ST, true, false>(a) : launch_one<D, P, F, ST, false, false>(a);
 }
 
+// DOGIP_STORE_FULL of the weighted projection runs the symmetry-adapted body (RefElem<.., 6>:
+// the same a_{T,j}, rows in orbit order) where it is instantiated: 3D p >= 3 (C5)
+template <int D, int P>
+__host__ __device__ constexpr bool full_sym_body() { return DOGIP_FULL_SYM && D == 3 && P >= 3; }
+
 template <int D, int P>
 cudaError_t launch_form(const ApplyArgs& a) {
     // every storage has the Dirichlet-elimination instantiation (DOGIP_DIRICHLET_ZERO)
     if (a.form == 0 && a.store == 2)
         return a.dirichlet ? launch_one<D, P, 0, 0, true, true>(a) : launch_one<D, P, 0, 0, false, true>(a);
     if (a.form == 0 && a.store == 5) return launch_dir<D, P, 0, 5>(a);
+    if (a.form == 0 && a.store == 6) {   // internal: FULL weights in orbit order, symmetry-adapted body
+        if constexpr (full_sym_body<D, P>()) return launch_dir<D, P, 0, 6>(a);
+        else return cudaErrorInvalidValue;
+    }
     if (a.form == 0) return launch_dir<D, P, 0, 0>(a);
     return a.store == 1 ? launch_dir<D, P, 1, 1>(a) : launch_dir<D, P, 1, 0>(a);
 }

@@ -190,12 +190,13 @@ __global__ void finalize_kernel(WeightsArgs a, int64_t e0, int64_t nb, int direc
         double ab[6];
         for (int c = 0; c < nc; ++c)
             ab[c] = direct ? adet * cconst[c] * a.sW[j] : a.scratch_a[(size_t)j * nb * nc + el * nc + c];
+        const int row = a.rowperm ? a.rowperm[j] : j;   // FULL WP with the symmetry-adapted body: orbit order
         if (!G.valid) {
-            for (int c = 0; c < NC; ++c) out[(size_t)(j * NC + c) * TILE] = 0.0;
+            for (int c = 0; c < NC; ++c) out[(size_t)(row * NC + c) * TILE] = 0.0;
             continue;
         }
         if (a.form == DOGIP_WP) {
-            out[(size_t)j * TILE] = ab[0];
+            out[(size_t)row * TILE] = ab[0];
             continue;
         }
         // Abar (symmetric) -> A = Rinv Abar Rinv^T  (A_rs = Rinv_rp Abar_pq Rinv_sq)
