@@ -106,13 +106,15 @@ def test_full_size_wp_total_c5():
         assert abs(t - ref) <= TOL * abs(ref), (store, t, ref)
 
 
-@pytest.mark.parametrize("d,N,p,form", [(3, 5, 3, 1), (2, 40, 2, 0)])
+@pytest.mark.parametrize("d,N,p,form", [(3, 5, 3, 1), (2, 40, 2, 0), (3, 4, 4, 0)])
 def test_negative_control_weight_perturbation(d, N, p, form):
     """A 1e-6 (relative) change of ONE stored weight entry must fail the parity bar; the
-    bar is therefore sensitive to single-entry errors in the streamed A_T."""
+    bar is therefore sensitive to single-entry errors in the streamed A_T.  (3, 4, 4, 0):
+    FULL WP storage with its rows in orbit order (the symmetry-adapted body), so the hook,
+    the export and the kernel must agree on the row permutation."""
     torch = _torch()
     from paper_1710_09913_b200.api import Mesh, Operator
-    c = get_config("C4" if form == 1 else "C1").with_size(N, p)
+    c = get_config("C4" if form == 1 else "C5" if d == 3 else "C1").with_size(N, p)
     coef = c.coefficient()
     m = Mesh(d, N, p)
     op = Operator(m, form, coef)
