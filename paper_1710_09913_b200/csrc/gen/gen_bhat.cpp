@@ -34,11 +34,17 @@ static std::string lit(double v) {
 
 static int g_split = 0;   // rows with >= g_split terms use two interleaved partial sums (argv[3]; 0 = off)
 
+// symmetry-adapted bodies read v through DOGIP_SYM_V(k, slot) (src "V"): registers by default,
+// or the u_T staging slot `slot` in shared memory (DOGIP_SYM_VSMEM A/B builds)
+static const std::vector<int>* g_vslot = nullptr;
+
 static std::string chain(const std::vector<std::pair<int, Rat>>& terms, const char* src, int& flops) {
     bool first = true;
     std::string acc;   // a chain of fma for determinism and contraction control
     for (auto& t : terms) {
-        const std::string src_l = std::string(src) + "[" + std::to_string(t.first) + "]";
+        const std::string src_l = (std::string(src) == "V" && g_vslot)
+            ? "DOGIP_SYM_V(" + std::to_string(t.first) + ", " + std::to_string((*g_vslot)[t.first]) + ")"
+            : std::string(src) + "[" + std::to_string(t.first) + "]";
         const Rat& c = t.second;
         if (first) {
             if (c == Rat(1)) acc = src_l;
@@ -454,7 +460,11 @@ static void emit_sym(FILE* f, int d, int p, bool raw = false) {
     int flops = 0;
     // 1. adapted coordinates v[k] = sum_{cosets} chi(c) u_{c l0} (stabiliser multiplicity
     //    folded into the block constants): butterflies over the generators
-    std::fprintf(f, "        double v[%d], z[%d];\n", VT, VT);
+    std::fprintf(f, "        DOGIP_SYM_VDECL(%d);\n        double z[%d];\n", VT, VT);
+    // v index -> u_T slot of the same orbit (read-all-then-write per orbit, so v can
+    // overwrite u in place when it lives in the shared-memory staging buffer)
+    static std::vector<int> vslot;
+    vslot.assign(VT, -1);
     auto coset_sum = [&](const Orb& o, int c, int gen_bits, const std::vector<std::vector<int>>& gx) {
         // distinct members with their sign: sum over e of chi(c,e) x_{e rep}, distinct only
         std::vector<std::pair<int, int>> terms;
@@ -472,24 +482,32 @@ static void emit_sym(FILE* f, int d, int p, bool raw = false) {
         const Orb& O = OV[o];
         const int sz = (int)O.members.size();
         if (sz == 1) {
-            std::fprintf(f, "        v[%d] = u[%d];\n", vidx[o][0], O.rep);
+            vslot[vidx[o][0]] = O.rep;
+            std::fprintf(f, "        DOGIP_SYM_VSET(%d, %d, DOGIP_SYM_U(%d));\n", vidx[o][0], O.rep, O.rep);
             continue;
         }
         if (sz == 2) {
             auto tm = coset_sum(O, 0, 0, gV);
-            std::fprintf(f, "        v[%d] = u[%d] + u[%d];\n", vidx[o][0], tm[0].first, tm[1].first);
-            std::fprintf(f, "        v[%d] = u[%d] - u[%d];\n", vidx[o][1], tm[0].first, tm[1].first);
+            const int a = tm[0].first, b = tm[1].first;
+            vslot[vidx[o][0]] = a;
+            vslot[vidx[o][1]] = b;
+            std::fprintf(f, "        { const double ua = DOGIP_SYM_U(%d), ub = DOGIP_SYM_U(%d);\n", a, b);
+            std::fprintf(f, "          DOGIP_SYM_VSET(%d, %d, ua + ub);\n", vidx[o][0], a);
+            std::fprintf(f, "          DOGIP_SYM_VSET(%d, %d, ua - ub);\n        }\n", vidx[o][1], b);
             flops += 2;
             continue;
         }
         // size 4: members a = e0, b = g1 a, c = g2 a, d = g1 g2 a; chars (s1, s2)
         const int a = gV[0][O.rep], b = gV[1][O.rep], c = gV[2][O.rep], dd = gV[3][O.rep];
-        std::fprintf(f, "        { const double tp = u[%d] + u[%d], tm = u[%d] - u[%d], rp = u[%d] + u[%d], rm = u[%d] - u[%d];\n",
-                     a, b, a, b, c, dd, c, dd);
+        const int mem[4] = {a, b, c, dd};
+        std::fprintf(f, "        { const double ua = DOGIP_SYM_U(%d), ub = DOGIP_SYM_U(%d), uc = DOGIP_SYM_U(%d), ud = DOGIP_SYM_U(%d);\n",
+                     a, b, c, dd);
+        std::fprintf(f, "          const double tp = ua + ub, tm = ua - ub, rp = uc + ud, rm = uc - ud;\n");
         for (size_t ci = 0; ci < O.chars.size(); ++ci) {
             const int ch = O.chars[ci];
             const bool s1 = ch & 1, s2 = ch & 2;   // chi(g1) = -1 if bit 0, chi(g2) = -1 if bit 1
-            std::fprintf(f, "          v[%d] = %s %s %s;\n", vidx[o][ci], s1 ? "tm" : "tp", s2 ? "-" : "+", s1 ? "rm" : "rp");
+            vslot[vidx[o][ci]] = mem[ci];
+            std::fprintf(f, "          DOGIP_SYM_VSET(%d, %d, %s %s %s);\n", vidx[o][ci], mem[ci], s1 ? "tm" : "tp", s2 ? "-" : "+", s1 ? "rm" : "rp");
         }
         std::fprintf(f, "        }\n");
         flops += 8;
@@ -544,7 +562,9 @@ static void emit_sym(FILE* f, int d, int p, bool raw = false) {
                 // -> ghat = sum_O (sum_{l in O} chi B[j0,l]) |H_O| v = sum_O sum_g chi(g) B[j0, g l0] v
                 if (!sum.is_zero()) terms.push_back({vidx[o][cpos], sum});
             }
-            flops += emit_combo(f, "          ", "g" + std::to_string(ci), true, terms, "v");
+            g_vslot = &vslot;
+            flops += emit_combo(f, "          ", "g" + std::to_string(ci), true, terms, "V");
+            g_vslot = nullptr;
         }
         // hhat_chi = sum_chi' ahat_{chi chi'} ghat_chi'  (ahat rows of this orbit)
         for (size_t ci = 0; ci < PO.chars.size(); ++ci) {
@@ -621,8 +641,9 @@ static void emit_sym(FILE* f, int d, int p, bool raw = false) {
             flops += (int)O.chars.size();
         }
     }
-    std::fprintf(f, "        if (dot) {\n          double s = 0.0;\n#pragma unroll\n"
-                    "          for (int k = 0; k < %d; ++k) s = fma(v[k], z[k], s);\n          *dot += s;\n        }\n", VT);
+    std::fprintf(f, "        if (dot) {\n          double s = 0.0;\n");
+    for (int k = 0; k < VT; ++k) std::fprintf(f, "          s = fma(DOGIP_SYM_V(%d, %d), z[%d], s);\n", k, vslot[k], k);
+    std::fprintf(f, "          *dot += s;\n        }\n");
     std::fprintf(f, "    }\n");
     std::fprintf(f, "    static constexpr int FLOPS = %d;\n", flops);
     std::fprintf(f, "};\n\n");
@@ -868,6 +889,13 @@ int main(int argc, char** argv) {
         "//   LOFF[s][l][a] = DoF-lattice offset (axis a) of local DoF l of simplex s\n"
         "//                   inside its cell, in units of the DoF lattice.\n"
         "#pragma once\n\n"
+        "// v of the symmetry-adapted bodies: registers unless the includer defines these\n"
+        "#ifndef DOGIP_SYM_VDECL\n"
+        "#define DOGIP_SYM_VDECL(n) double v[n]\n"
+        "#define DOGIP_SYM_VSET(k, slot, e) (v[k] = (e))\n"
+        "#define DOGIP_SYM_V(k, slot) v[k]\n"
+        "#define DOGIP_SYM_U(l) u[l]\n"
+        "#endif\n\n"
         "namespace dogip_gen {\n\n"
         "template <int D, int P, int FORM, int STORE> struct RefElem;\n\n");
     for (int d = 2; d <= 3; ++d)

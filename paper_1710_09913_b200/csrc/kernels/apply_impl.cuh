@@ -39,6 +39,25 @@
 
 #include <cstdlib>
 
+#include <cstdint>
+#ifndef DOGIP_SYM_VSMEM
+#define DOGIP_SYM_VSMEM 0      // 1: the symmetry-adapted body keeps v in the u_T staging buffer in shared
+                               // memory (not registers), at 3 CTAs/SM (A/B builds)
+#endif
+#if DOGIP_SYM_VSMEM
+__device__ __forceinline__ double dogip_lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void dogip_sts_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v));
+}
+#define DOGIP_SYM_VDECL(n) const uint32_t vs_ = pol.vs
+#define DOGIP_SYM_VSET(k, slot, e) dogip_sts_f64(vs_ + 256u * (slot), (e))
+#define DOGIP_SYM_V(k, slot) dogip_lds_f64(vs_ + 256u * (slot))
+#define DOGIP_SYM_U(l) dogip_lds_f64(vs_ + 256u * (l))
+#endif
 #ifdef DOGIP_GEN_HEADER
 #include DOGIP_GEN_HEADER
 #else
@@ -95,6 +114,7 @@ constexpr int min_blocks() {
 #endif
     // 2D P4 (V_T = 15): 2 CTAs / 255 registers beat 3 / 168 with spills (C2 p=4 -4 %, iso -5 %,
     // profiles/r02_ab_minb.log)
+    if (DOGIP_SYM_VSMEM && RE::DOT_IN_BODY) return 3;
     return RE::VT <= 10 ? DOGIP_MINB_SMALL : (RE::VT <= 20 && RE::NS == 6) ? 3 : DOGIP_MINB_LARGE;
 }
 
@@ -164,6 +184,7 @@ struct WarpStream {
     uint32_t cons;         // chunks consumed so far (stage = cons % S, parity = cons / S)
     const double* cur;     // current stage + lane
     uint64_t policy;
+    uint32_t vs;           // DOGIP_SYM_VSMEM: smem address of this lane's u_T / v column
 
     // chunk-sequence number g (relative: K tiles ahead, chunk c) -> stage g % S
     template <int K, int CI>
@@ -542,6 +563,32 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
         for (int64_t tile = gw; tile < tile_end; tile += nw) {
             cp_async_wait_all();
             __syncwarp();
+#if DOGIP_SYM_VSMEM
+            {
+            // v lives in this lane's staging column: zero the slots the gather skipped, run
+            // the body on smem, then stage the next tile (after the body's last v read)
+            if (!cur.valid || cur.skip) {
+#pragma unroll
+                for (int l = 0; l < RE::VT; ++l)
+                    if (!cur.valid || ((cur.skip >> l) & 1ull)) dogip_sts_f64(ubuf_lane + 256u * l, 0.0);
+            }
+            const ElemCtx prev = cur;
+            double yT[RE::VT];
+#pragma unroll
+            for (int l = 0; l < RE::VT; ++l) yT[l] = 0.0;
+            ws.vs = ubuf_lane;
+            RE::body(nullptr, yT, ws, dot_partials ? &udot : nullptr);
+            ws.next_tile();
+            __syncwarp();
+            if (tile + nw < tile_end) {
+                cur = elem_ctx<RE, D, DIR>(geo, tab, tile + nw, lane);
+                gather_async<RE>(u, cur, ubuf_lane);
+            }
+            cp_async_commit();
+            if (prev.valid) scatter<RE>(y, prev, yT);
+            continue;
+            }
+#endif
 #pragma unroll
             for (int l = 0; l < RE::VT; ++l)
                 uT[l] = (cur.valid && !((cur.skip >> l) & 1ull)) ? ubuf[l * TILE + lane] : 0.0;
