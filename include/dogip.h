@@ -76,7 +76,10 @@ extern "C" {
 #define DOGIP_COEF_CONST_TENSOR   5  /* M = params[0..d*d) row-major, symmetric (EL only)   */
 
 /* ---- weight storage (dogip_weights_ex) ---------------------------------- */
-#define DOGIP_STORE_FULL  0  /* WP: a_{T,j}; EL: symmetric A_{T,j} (d(d+1)/2 per node)    */
+#define DOGIP_STORE_FULL  0  /* WP: a_{T,j}; EL: symmetric A_{T,j} (d(d+1)/2 per node).
+                                The device layout is internal (3D WP p >= 3: node rows in the
+                                orbit order of DOGIP_STORE_SYM, applied through the same
+                                block-diagonal body); dogip_export_weights returns canonical order */
 #define DOGIP_STORE_ISO   1  /* EL with isotropic M = m I (Corollary, element-wise):
                                 A_{T,j} = a_{T,j} G_T, a_{T,j} = int_T m phi^W_j, G_T = Rinv Rinv^T;
                                 stores W_T + d(d+1)/2 doubles per element instead of W_T d(d+1)/2 */
@@ -91,8 +94,9 @@ extern "C" {
                                 the double-grid nodes under the barycentric involutions
                                 G = <(0 1), (2 3)> (3D) / <(0 1)> (2D), ahat_psi(P) = (1/|G|) sum_g
                                 psi(g) a_{g j0}; the apply runs Bhat block-diagonally by character
-                                (3D P4: 784 instead of 1729 nonzeros); same bytes, ~1/3 fewer FP64
-                                operations than DOGIP_STORE_FULL */
+                                (3D P4: 784 instead of 1729 nonzeros); same bytes; in 3D p >= 3
+                                DOGIP_STORE_FULL runs the same body on the plain values (~10 %
+                                more FP64 operations than this storage) */
 #define DOGIP_STORE_QP     4 /* no DoGIP weights: the quadrature-point matrix-free comparator
                                 ("alternative approaches") -- geometry, coefficient and the
                                 basis contractions at the n_q points of the contract rule (L10) are
