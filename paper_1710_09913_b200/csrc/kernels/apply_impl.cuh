@@ -108,7 +108,7 @@ namespace {
 #define DOGIP_ROWS_4CTA 12
 #endif
 template <class RE>
-constexpr int min_blocks() {
+constexpr int min_blocks128() {   // CTAs of APPLY_THREADS (4 warps) per SM
 #ifdef DOGIP_MINB_OVERRIDE
     return DOGIP_MINB_OVERRIDE;
 #endif
@@ -116,6 +116,23 @@ constexpr int min_blocks() {
     // profiles/r02_ab_minb.log)
     if (DOGIP_SYM_VSMEM && RE::DOT_IN_BODY) return 3;
     return RE::VT <= 10 ? DOGIP_MINB_SMALL : (RE::VT <= 20 && RE::NS == 6) ? 3 : DOGIP_MINB_LARGE;
+}
+
+// Threads per CTA.  The symmetry-adapted bodies at 8 warps/SM (3D P4 WP: SYM, and FULL through
+// the same body) run as ONE 8-warp CTA per SM instead of two 4-warp CTAs: the SM's warps then
+// hold 8 consecutive tiles (the Kuhn types of the same cells, then the next x-block), so
+// their u_T gathers and y atomics share L1 / L2 lines (C5 SYM 1.76 -> 1.69 ms, FULL 1.90 ->
+// 1.79 median, profiles/r02_ab_cta256.log).  The other kernels measured neutral or slower.
+#ifndef DOGIP_SYM_CTA8
+#define DOGIP_SYM_CTA8 1
+#endif
+template <class RE>
+__host__ __device__ constexpr int cta_threads() {
+    return (DOGIP_SYM_CTA8 && RE::DOT_IN_BODY && min_blocks128<RE>() == 2) ? 2 * APPLY_THREADS : APPLY_THREADS;
+}
+template <class RE>
+constexpr int min_blocks() {       // CTAs of cta_threads<RE>() per SM asked of ptxas
+    return min_blocks128<RE>() * APPLY_THREADS / cta_threads<RE>();
 }
 
 // Balanced chunks of whole nodes: NCH = ceil(TILE_ROWS / ROWS_MAX) chunks of ROWS rows
@@ -211,7 +228,7 @@ struct WarpStream {
         constexpr int c_cur = RE::row_of(J) / C::ROWS;
         if constexpr (J == 0 || c_cur != RE::row_of(J - 1) / C::ROWS) {
             constexpr int gi = c_cur + C::S - 1;          // chunk refilled now, relative to this tile
-            if constexpr (lockstep<RE>()) asm volatile("bar.sync 1, %0;" ::"n"(APPLY_THREADS) : "memory");
+            if constexpr (lockstep<RE>()) asm volatile("bar.sync 1, %0;" ::"n"(cta_threads<RE>()) : "memory");
             __syncwarp();
             if (lane == 0) {
                 fence_proxy_async_smem();                 // prior generic reads of the stage
@@ -256,7 +273,7 @@ __device__ __forceinline__ void lockstep_tail(int64_t gw, int64_t tile_end, int6
         const int64_t mine = gw < tile_end ? (tile_end - gw + nw - 1) / nw : 0;
         const int64_t first = gw0 < tile_end ? (tile_end - gw0 + nw - 1) / nw : 0;
         for (int64_t k = mine; k < first; ++k)
-            for (int c = 0; c < C::NCH; ++c) asm volatile("bar.sync 1, %0;" ::"n"(APPLY_THREADS) : "memory");
+            for (int c = 0; c < C::NCH; ++c) asm volatile("bar.sync 1, %0;" ::"n"(cta_threads<RE>()) : "memory");
     }
 }
 
@@ -465,11 +482,11 @@ __device__ __forceinline__ uint64_t pair_combine(double* yT, double* buf, int pa
 // profiles/r02_ab_pair_combine.log
 template <class RE, int D, int F>
 __host__ __device__ constexpr bool pair_enabled() {
-    return DOGIP_PAIR_COMBINE && D == 3 && F == 1 && !direct_weights<RE>() && APPLY_THREADS % 64 == 0;
+    return DOGIP_PAIR_COMBINE && D == 3 && F == 1 && !direct_weights<RE>() && cta_threads<RE>() % 64 == 0;
 }
 
 template <int D, int P, int F, int ST, bool DIR, bool GLOB>
-__global__ void __launch_bounds__(APPLY_THREADS, min_blocks<dogip_gen::RefElem<D, P, F, ST>>())
+__global__ void __launch_bounds__(cta_threads<dogip_gen::RefElem<D, P, F, ST>>(), min_blocks<dogip_gen::RefElem<D, P, F, ST>>())
 apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double* __restrict__ w,
              const SlabGeo geo, const ApplyTables tab, const int64_t tile_begin, const int64_t tile_end,
              double* __restrict__ dot_partials, const int* __restrict__ offw_g,
@@ -477,7 +494,7 @@ apply_kernel(const double* __restrict__ u, double* __restrict__ y, const double*
     if (skip_if && *skip_if != 0.0) return;    // finished CG solve: the weight stream is not read
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
-    constexpr int NW = APPLY_THREADS / 32;
+    constexpr int NW = cta_threads<RE>() / 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr bool RING = !(GLOB || direct_weights<RE>());                   // weight ring + mbarriers
     double* rings = reinterpret_cast<double*>(smem_raw);
@@ -655,7 +672,7 @@ template <int D, int P, int F, int ST, bool DIR, bool GLOB>
 cudaError_t launch_one(const ApplyArgs& a) {
     using RE = dogip_gen::RefElem<D, P, F, ST>;
     using C = Chunking<RE>;
-    constexpr int NW = APPLY_THREADS / 32;
+    constexpr int NW = cta_threads<RE>() / 32;
     constexpr bool UPF = DOGIP_SYM_UPF && RE::DOT_IN_BODY && !GLOB;
     constexpr bool DW = direct_weights<RE>() && !GLOB;
     const size_t smem = ((GLOB || DW) ? 0 : (size_t)NW * C::S * C::ROWS * TILE * 8 + (size_t)NW * C::S * 8) +
@@ -664,7 +681,7 @@ cudaError_t launch_one(const ApplyArgs& a) {
     auto kern = apply_kernel<D, P, F, ST, DIR, GLOB>;
     static std::atomic<uint64_t> cfg[MAX_DEVICES];   // per instantiation, per device
     int occ = 1;
-    if (cudaError_t e = kernel_occupancy(kern, APPLY_THREADS, smem, cfg, &occ); e != cudaSuccess) return e;
+    if (cudaError_t e = kernel_occupancy(kern, cta_threads<RE>(), smem, cfg, &occ); e != cudaSuccess) return e;
     const int64_t ntiles = a.tile_end - a.tile_begin;
     int64_t grid = (int64_t)a.num_sms * occ;
     const int64_t need = (ntiles + NW - 1) / NW;
@@ -676,7 +693,7 @@ cudaError_t launch_one(const ApplyArgs& a) {
     } else if (ntiles <= 0) {
         return cudaSuccess;
     }
-    kern<<<(unsigned)grid, APPLY_THREADS, smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, a.tile_begin,
+    kern<<<(unsigned)grid, cta_threads<RE>(), smem, a.stream>>>(a.u, a.y, a.w, a.geo, *a.tab, a.tile_begin,
                                                            a.tile_end, a.dot_partials, a.offw, a.skip_if);
     count_launches(1);
     return cudaGetLastError();
