@@ -12,7 +12,7 @@ and applies A by the quadrature-point route (oracle.assemble.apply_qp_route, pin
 to the CSR assembly in tests/test_oracle_sampled_and_coefficients.py); nothing on that side
 comes from the CUDA path except the solution x under test.
 
-    python scripts/oracle_residual.py [--out gpurun_out/r02_oracle_residual.json] [C3 C5]
+    python tests/oracle_residual.py [--out gpurun_out/r02_oracle_residual.json] [C3 C5]
 """
 from __future__ import annotations
 
