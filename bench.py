@@ -570,7 +570,7 @@ def run_product(args, cfg) -> None:
                "e2e": {"value": info["ndof_global"] / t_e2e.item() / 1e9, "unit": UNIT,
                        "h2d_bytes_per_step": int(tot_vec.item()), "d2h_bytes_per_step": int(tot_vec.item()),
                        "api": "dogip_apply_host (pinned host u -> device, apply, device -> host y; "
-                              "pipelined over 16 chunks of cube layers on copy-in / compute / copy-out "
+                              "pipelined over 24 chunks of cube layers on copy-in / compute / copy-out "
                               "streams when single-rank)"},
                "e2e_cg": {"value": info["ndof_global"] / t_cg_e2e / 1e9, "unit": UNIT,
                           "s_per_iter": t_cg_e2e, "iters": kc,

@@ -280,7 +280,7 @@ int dogip_apply(dogip_op op, const double* u, double* y, unsigned flags, void* s
 /*
  * dogip_apply_host -- the same apply with HOST buffers u_host, y_host (ndof_local
  * doubles each, caller-owned; pinned memory is needed for the copies to overlap).
- * Single rank: pipelined over up to 16 chunks of cube layers along the slab axis --
+ * Single rank: pipelined over up to 24 chunks of cube layers along the slab axis --
  * copy-in of the next chunk's u planes, the apply kernel of this chunk's elements and
  * copy-out of the y planes it completed run concurrently on three streams (library-
  * owned device scratch and copy streams, ordered after prior work on `stream`).
