@@ -149,13 +149,13 @@ def oracle_sample_apply(cfg, n_cells: int, seed_offset: int = 0):
     M = N + 1
     vids = np.unique(elems)
     vlat = np.stack([(vids // M ** a) % M for a in range(d)], axis=1)
-    verts = _ORACLE_CACHE.setdefault(cfg.name + "v", cfg.vertices())
+    verts = _cached(cfg.name + "v", cfg.vertices)
     X = vlat / N if verts is None else verts[vids]
     remap = np.full(vids.max() + 1, -1, dtype=np.int64)
     remap[vids] = np.arange(vids.size)
     sub = Mesh(d, N, vlat, X, remap[elems], np.repeat(cells, 2 if d == 2 else 6))
-    coef = _ORACLE_CACHE.setdefault(cfg.name, cfg.coefficient())
-    u = _ORACLE_CACHE.setdefault(cfg.name + "u", cfg.u())
+    coef = _cached(cfg.name, cfg.coefficient)
+    u = _cached(cfg.name + "u", cfg.u)
     t0 = time.perf_counter()
     ed = ElementData(sub, p)
     form = cfg.forms[0]
@@ -169,6 +169,13 @@ def oracle_sample_apply(cfg, n_cells: int, seed_offset: int = 0):
 
 
 _ORACLE_CACHE: dict = {}
+
+
+def _cached(key, make):
+    """Seeded inputs of the workload, generated once per process (forked workers inherit them)."""
+    if key not in _ORACLE_CACHE:
+        _ORACLE_CACHE[key] = make()
+    return _ORACLE_CACHE[key]
 _POOL_CFG = None
 
 
@@ -193,18 +200,20 @@ def _blas_vendor() -> str:
         return f"unknown ({e})"
 
 
-def oracle_parallel_sample(cfg, target_s: float, offset0: int = 0):
+def oracle_parallel_sample(cfg, target_s: float, offset0: int = 0, n_cells: int | None = None):
     """The oracle as it stands, on every host core: one worker process per core, each
     running the element route on its own block of consecutive cells (disjoint blocks),
-    about target_s seconds of work per worker.  Returns (elements, wall seconds, cores,
-    per-worker elements)."""
+    about target_s seconds of work per worker (n_cells given: that many cells per worker,
+    no calibration run).  Returns (elements, wall seconds, cores, per-worker elements)."""
     global _POOL_CFG
     import multiprocessing as mp
     cores = _cores()
     oracle_sample_apply(cfg, 8)                                    # imports, caches (inherited by fork)
-    ne, t = oracle_sample_apply(cfg, 128)
-    per_cell = t / (128)
-    n_cells = int(max(16, min(cfg.N ** cfg.d // max(1, cores), target_s / per_cell)))
+    if n_cells is None:
+        ne, t = oracle_sample_apply(cfg, 128)
+        per_cell = t / (128)
+        n_cells = int(target_s / per_cell)
+    n_cells = int(max(16, min(cfg.N ** cfg.d // max(1, cores), n_cells)))
     _POOL_CFG = cfg
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
@@ -278,15 +287,19 @@ def run_reference(args, cfg) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    per_step_target = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
-    for w in range(args.warmup):
-        oracle_parallel_sample(cfg, per_step_target, w)
+    per_step_target = max(1.0, min(8.0, 100.0 / max(1, args.steps + args.warmup)))
+    # the sample size follows the measured wall time of the previous step (workers share the
+    # host's memory bandwidth, so the one-process calibration under-estimates a step)
+    n_cells = None
+    per_elem_cells = 2 if cfg.d == 2 else 6
     walls, nes = [], []
     cores, per = _cores(), 0
-    for k in range(args.steps):
-        ne, wall, cores, per = oracle_parallel_sample(cfg, per_step_target, args.warmup + k)
-        walls.append(wall)
-        nes.append(ne)
+    for k in range(args.warmup + args.steps):
+        ne, wall, cores, per = oracle_parallel_sample(cfg, per_step_target, k, n_cells)
+        n_cells = max(16, int(per // per_elem_cells * min(2.0, max(0.25, per_step_target / max(wall, 1e-3)))))
+        if k >= args.warmup:
+            walls.append(wall)
+            nes.append(ne)
     tot = sum(walls)
     frac = sum(nes) / cfg.n_elem
     value = cfg.ndof * frac / tot / 1e9
@@ -295,8 +308,10 @@ def run_reference(args, cfg) -> None:
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": _config_dict(cfg, args.gpus),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "blas": _blas_vendor(),
-                            "sample": f"each step: oracle element-route apply over {nes[0]} elements "
-                                      f"({cores} processes x {per} elements of consecutive cells) of {cfg.name}"},
+                            "sample": f"each step: oracle element-route apply over {min(nes)}-{max(nes)} elements "
+                                      f"({cores} processes x disjoint blocks of consecutive cells, sized from the "
+                                      f"previous step's wall time for ~{per_step_target:.1f} s per step; "
+                                      f"{sum(nes)} elements over the timed steps) of {cfg.name}"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
